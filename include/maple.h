@@ -1,0 +1,182 @@
+/*
+ * maple.h — C ABI of the B200-native MAPLE hot path (arXiv 2412.13576, "GPU-based Graver Basis
+ * Extraction for Nonlinear Integer Optimization").
+ *
+ * Problem (model (1)):  min f(x)  s.t.  A x = b,  l <= x <= u,  x in Z^n,
+ * with A in Z^{m x n} of full row rank m < n. A, l, u are shared by every call on a context; f and b vary
+ * per augmentation call (the paper's "flexibility").
+ *
+ * Conventions (all entry points):
+ *  - Return value: 0 (MAPLE_OK) or a negative MAPLE_ERR_* code; no C++ exception crosses the ABI.
+ *    maple_last_error(ctx) then holds a one-line human-readable reason.
+ *  - Pointers documented "host" are ordinary host memory; "device" are CUDA device pointers on the
+ *    context's device. Every input is copied (the caller may free it on return) unless stated.
+ *  - Matrices are dense row-major int32 / float64 unless stated. Sizes are element counts.
+ *  - Work is enqueued on the context's stream (maple_set_stream; default: the legacy default stream) and
+ *    every call that returns host data synchronises that stream before returning.
+ *  - A context is not thread-safe; distinct contexts are independent. One context = one device.
+ *  - Determinism: for a fixed (A, l, u, parameters, seed) every result is bit-identical across runs and
+ *    across any partition of the starts into ranges (maple_extract_range), i.e. across 1..8 GPUs.
+ */
+#ifndef MAPLE_H
+#define MAPLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------------------------------- */
+#define MAPLE_OK                   0
+#define MAPLE_ERR_BAD_ARG         -1   /* null pointer, bad size, lambda < 0, N < 1, T < 1, lr <= 0 ... */
+#define MAPLE_ERR_BAD_BOUNDS      -2   /* some l_i > u_i (SPEC S:243 BadBounds) */
+#define MAPLE_ERR_RANK_DEFICIENT  -3   /* rank(A) < m */
+#define MAPLE_ERR_FULL_RANK       -4   /* m >= n: Ker_Z(A) = {0} */
+#define MAPLE_ERR_OVERFLOW        -5   /* exact host integer arithmetic (checked __int128) overflowed */
+#define MAPLE_ERR_RANGE           -6   /* a value does not fit the device encoding (|B_ij| > 127,
+                                          max(u-l) > 127, n > MAPLE_MAX_N, ...) */
+#define MAPLE_ERR_CUDA            -7   /* a CUDA runtime call or kernel failed */
+#define MAPLE_ERR_OOM             -8   /* device allocation failed */
+#define MAPLE_ERR_CAPACITY        -9   /* a device set outgrew its hard cap */
+#define MAPLE_ERR_INFEASIBLE     -10   /* an x0 row violates A x = b or l <= x <= u */
+#define MAPLE_ERR_COMM           -11   /* reserved for the multi-GPU merge (collectives run in the caller) */
+
+/* augmentation status (not an error) */
+#define MAPLE_STATUS_OK            0
+#define MAPLE_STATUS_NO_FEASIBLE   1   /* k0 == 0: no incumbent to augment */
+
+/* objective kinds for maple_objective.kind */
+#define MAPLE_OBJ_QUADRATIC        0   /* f(x) = 1/2 x^T Q x + c^T x + c0, Q dense n x n */
+#define MAPLE_OBJ_SEPARABLE        1   /* same with Q diagonal: Q points to the n diagonal entries */
+
+#define MAPLE_MAX_N             1024   /* device row encoding limit on n */
+
+typedef struct maple_ctx maple_ctx;
+typedef struct maple_dirset maple_dirset;
+
+typedef struct maple_objective {
+    int32_t kind;          /* MAPLE_OBJ_QUADRATIC or MAPLE_OBJ_SEPARABLE */
+    const double* Q;       /* host; n*n row-major (QUADRATIC) or n (SEPARABLE); must be symmetric */
+    const double* c;       /* host; n */
+    double c0;
+} maple_objective;
+
+/* ---- context ------------------------------------------------------------------------------------
+ * maple_create — Alg. 3 lines 2-3 and the Remark on B^{-1}, run once per A:
+ *   HNF  A C = (H | 0) with C unimodular (Prop. 1) in checked __int128 arithmetic;
+ *   B = C[:, m:] (Thm. 1: Ker_Z(A) = L(B));  B <- LLL(B) with the paper's Siegel condition
+ *   ||B*_{k-1}||^2 <= 2 ||B*_k||^2 (Def. P:136-144, Alg. 1);  B+ = (B^T B)^{-1} B^T in fp64;
+ *   A B = 0 re-verified exactly; then A, B (int8 + fp32 copies), B+ and the box M = [l-u, u-l]
+ *    are uploaded to `device`.
+ * A: host int32 m*n row-major.  l, u: host int32 n.  device: CUDA ordinal.  out: receives the context,
+ * owned by the library until maple_destroy.
+ * Errors: BAD_ARG, BAD_BOUNDS, RANK_DEFICIENT, FULL_RANK, OVERFLOW, RANGE, CUDA, OOM.              */
+int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const int32_t* u, int device,
+                 maple_ctx** out);
+void maple_destroy(maple_ctx* ctx);
+
+/* Host-only part of maple_create (no device needed): the reduced kernel basis B (host int32 n x d
+ * row-major, d = n - m) and, if Bp_out != NULL, B+ (host fp64 d x n) exactly as maple_create computes
+ * them. Errors as maple_create minus CUDA/OOM. */
+int maple_kernel_basis(const int32_t* A, int32_t m, int32_t n, int32_t* B_out, double* Bp_out);
+
+/* Enqueue all further work on `stream` (a cudaStream_t, e.g. torch.cuda.current_stream().cuda_stream). */
+int maple_set_stream(maple_ctx* ctx, void* stream);
+
+/* Eq. 3 weights and Adam moments (reading #9): defaults lambda1 = 0.85, lambda2 = 1,
+ * beta1 = 0.9, beta2 = 0.999, eps = 1e-8. filter_minimal = 1 (north star: keep only ⊑-minimal rows,
+ * condition C4 P:283) or 0 (the paper's unfiltered pool). Errors: BAD_ARG (negative lambda,
+ * beta outside [0,1), eps <= 0). */
+int maple_set_extract_params(maple_ctx* ctx, double lambda1, double lambda2, double beta1, double beta2,
+                             double eps, int32_t filter_minimal);
+
+/* Copy the context's reduced kernel basis B (n x d, d = n - m, row-major) to host int32 `B_out`
+ * (n*d elements). B is not unique; this is the one every extraction on ctx uses. */
+int maple_get_basis(const maple_ctx* ctx, int32_t* B_out);
+/* Copy B+ (d x n, row-major fp64) to host. */
+int maple_get_pinv(const maple_ctx* ctx, double* Bp_out);
+int32_t maple_dim_n(const maple_ctx* ctx);
+int32_t maple_dim_d(const maple_ctx* ctx);
+const char* maple_last_error(const maple_ctx* ctx);
+
+/* ---- extraction ---------------------------------------------------------------------------------
+ * maple_extract — Algorithm 3 plus the north-star post-processing, all on the device:
+ *   starts i = 0..n_starts-1: g0 ~ U(l-u, u-l) from a splitmix64 counter keyed by (seed, i, j), z0 = B+ g0
+ *   (P:386); `steps` Adam steps (lr = step_size) on Eq. 3; after every step the
+ *   rounded iterate g = B round(z) (half away from zero) is harvested if g != 0 and g in M;
+ *   then the exact check A g = 0 (C1-C3), dedupe with sign twins collapsed (first nonzero > 0),
+ *   the ⊑-minimality filter (Def. 1-2; unless filter_minimal = 0) and a lexicographic sort.
+ * out: receives a direction set owned by the library until maple_dirset_free.
+ * Errors: BAD_ARG (n_starts < 1, steps < 1, step_size <= 0), CAPACITY, CUDA, OOM.                    */
+int maple_extract(maple_ctx* ctx, int64_t n_starts, int32_t steps, double step_size, uint64_t seed,
+                  maple_dirset** out);
+
+/* Same computation restricted to global start indices [begin, end) of an n_starts-start run (the RNG is
+ * keyed by the global index, so the union over any partition equals maple_extract's candidate set).
+ * Used for multi-GPU sharding: each rank extracts its range, the caller all-gathers the rows
+ * (torch.distributed / NCCL), then maple_dirset_merge runs the global dedupe + filter + sort. */
+int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
+                        double step_size, uint64_t seed, maple_dirset** out);
+
+/* Global pass over caller rows: `rows` is a DEVICE int8 buffer of k rows with row stride `stride`
+ * (>= n) bytes; rows are checked, deduped (with sign twins), filtered and sorted exactly like the tail
+ * of maple_extract. The buffer is only read during the call. */
+int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t stride, maple_dirset** out);
+
+/* Direction-set accessors: canonical rows (first nonzero > 0), lexicographically sorted, size x n. */
+int64_t maple_dirset_size(const maple_dirset* ds);
+int64_t maple_dirset_pool_size(const maple_dirset* ds);   /* unique checked rows before the ⊑ filter */
+int maple_dirset_copy(const maple_dirset* ds, int32_t* host_rows);            /* size*n int32, host */
+const int8_t* maple_dirset_device_rows(const maple_dirset* ds);   /* borrowed; stride maple_dirset_stride */
+/* Device-to-device copy of the size x stride int8 rows into caller memory `dst` (e.g. a torch tensor that
+ * feeds the NCCL all-gather); enqueued on the context stream and synchronised. */
+int maple_dirset_copy_device(const maple_dirset* ds, int8_t* dst);
+int32_t maple_dirset_stride(const maple_dirset* ds);
+void maple_dirset_free(maple_dirset* ds);
+
+/* Import host rows (k x n int32) as a direction set after the same check/dedupe/filter/sort. */
+int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32_t filter_minimal,
+                           maple_dirset** out);
+
+/* ---- augmentation -------------------------------------------------------------------------------
+ * maple_augment — Graver-best augmentation (Alg. 2) from each of the k0 incumbents x0 (host,
+ * k0 x n int32) in parallel, with test set D = ds ∪ -ds; each iteration takes the argmin of
+ * f(x + lambda g) over g in D, integer lambda in [1, lambda_max(x, g)] with x + lambda g in [l, u] and
+ * f(x + lambda g) < f(x) (ties: lexicographically smallest g, then smaller lambda), until no improving step
+ * exists; returns the best final incumbent (ties: lexicographically smallest x) — MAPLE's multi-start
+ * (§4.3). f is evaluated exactly via 2 f in fp64 (exact for integer data below 2^53).
+ * f: objective (host arrays). b: host int32 m. x_best: host int32 n (out). f_best: host (out).
+ * status: MAPLE_STATUS_*. iters (optional, host int32 k0, may be NULL): augmentation steps per incumbent.
+ * Errors: BAD_ARG, INFEASIBLE (some x0 violates A x = b or the box), CUDA, OOM.                     */
+int maple_augment(maple_ctx* ctx, const maple_dirset* ds, const maple_objective* f, const int32_t* b,
+                  const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best, int32_t* status,
+                  int32_t* iters);
+
+/* Batched shared-A augmentation (configs[3]): n_inst instances, instance t uses objective f[t],
+ * right-hand side b[t*m..], incumbents x0[t*k0*n..]; outputs x_best[t*n..], f_best[t]. */
+int maple_augment_many(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, const maple_objective* f,
+                       const int32_t* b, const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best);
+
+/* ---- instrumentation / parity hooks (used by tests and bench.py) -------------------------------
+ * maple_debug_descent: run only the descent of starts [begin, end) (no harvest side effects) and copy
+ * the final iterates (end-begin) x d fp32 to host `Z_out` (and, if Z0_out != NULL, the starts z0 in fp64).
+ * maple_debug_candidates: after the last maple_extract / maple_extract_range on ctx, copy the harvested
+ * candidate multiset (the rows handed to dedupe; in-box, nonzero, canonical) to host int32 rows; returns
+ * the row count (call with host_rows = NULL, cap = 0 to query). Enabled by maple_set_debug(ctx, 1).
+ * maple_last_timings: device milliseconds of the last extraction's phases
+ * [descent, dedupe, check, filter, sort, total] and of the last augmentation [precompute, iterate, total]. */
+int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
+                        double step_size, uint64_t seed, float* Z_out, double* Z0_out);
+int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates);
+int64_t maple_debug_candidates(maple_ctx* ctx, int32_t* host_rows, int64_t cap);
+int maple_last_timings(const maple_ctx* ctx, float* extract_ms6, float* augment_ms3);
+/* Number of CUDA kernel launches the library issued since the context was created. */
+int64_t maple_kernel_launches(const maple_ctx* ctx);
+/* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05. */
+int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPLE_H */

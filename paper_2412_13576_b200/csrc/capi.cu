@@ -1,0 +1,850 @@
+// C ABI of the MAPLE hot path (include/maple.h): context, extraction pipeline, merge, augmentation.
+// Host code here only orchestrates: every step of the path runs in the kernels of k_*.cu; the host
+// does the once-per-A exact lattice work of maple_create (lattice.cpp) and argument validation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/maple.h"
+#include "kernels.h"
+#include "lattice.h"
+
+using namespace maple;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        size_t b = std::max<size_t>(want, 256);
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
+inline uint64_t next_pow2(uint64_t v) {
+    uint64_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+struct maple_ctx {
+    int device = 0;
+    cudaStream_t stream = 0;
+    int m = 0, n = 0, d = 0, n_pad = 16;
+    std::vector<int32_t> A, l, u, box;
+    std::vector<int64_t> B;       // n x d
+    std::vector<double> Bp;       // d x n
+    // device constants
+    DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, bit_coord, bit_k;
+    int nnz = 0, Lh = 0, Wh = 0;
+    // params (Eq. 3 / Adam)
+    double lam1 = 0.85, lam2 = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+    int filter_minimal = 1;
+    int descent_kernel = 0;
+    // workspace
+    DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, l1, hist, level_start, cursor, order, keep,
+        witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
+    DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b;
+    int64_t cand_cap = 0, pool_cap = 0;
+    uint64_t table_slots = 0;
+    std::string err;
+    float t_extract[6] = {0, 0, 0, 0, 0, 0};
+    float t_augment[3] = {0, 0, 0};
+    int64_t launches = 0;
+    int debug_keep = 0;
+    std::vector<int8_t> dbg_cand;
+    int64_t dbg_count = 0;
+    cudaEvent_t ev[8] = {};
+};
+
+struct maple_dirset {
+    maple_ctx* ctx = nullptr;
+    int n = 0, n_pad = 16;
+    int64_t size = 0, pool_size = 0, n_bad = 0;
+    int8_t* rows = nullptr;       // size x n_pad, canonical, lex sorted
+    int8_t* D = nullptr;          // 2*size x n_pad: rows ∪ -rows, lex sorted (lazily built)
+};
+
+// counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
+enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_N = 6 };
+
+#define FAIL(code, msg)              \
+    do {                             \
+        if (ctx) ctx->err = (msg);   \
+        return (code);               \
+    } while (0)
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            if (ctx) ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                \
+            cudaGetLastError();                                                                    \
+            return e_ == cudaErrorMemoryAllocation ? MAPLE_ERR_OOM : MAPLE_ERR_CUDA;               \
+        }                                                                                          \
+    } while (0)
+
+namespace {
+
+template <class T>
+cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
+    cudaError_t e = b.ensure(std::max<size_t>(1, v.size()) * sizeof(T));
+    if (e != cudaSuccess) return e;
+    if (v.empty()) return cudaSuccess;
+    return cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+unsigned long long* counters(maple_ctx* c) { return c->counters.as<unsigned long long>(); }
+
+int read_counters(maple_ctx* ctx, unsigned long long* h) {
+    CU(cudaMemcpyAsync(h, ctx->counters.p, sizeof(unsigned long long) * C_N, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MAPLE_OK;
+}
+
+// (Re)build an empty hash set able to hold `cap` unique rows; existing pool rows are re-inserted.
+int ensure_set(maple_ctx* ctx, int64_t cap, bool keep_existing, int64_t existing) {
+    if (cap <= ctx->pool_cap) {
+        if (!keep_existing) {
+            CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
+            CU(cudaMemsetAsync(ctx->idx.p, 0xFF, ctx->table_slots * 4, ctx->stream));
+            CU(cudaMemsetAsync(counters(ctx) + C_POOL, 0, 8, ctx->stream));
+        }
+        return MAPLE_OK;
+    }
+    int64_t newcap = std::max<int64_t>(cap, std::max<int64_t>(4096, ctx->pool_cap * 2));
+    uint64_t slots = next_pow2((uint64_t)newcap * 2);
+    DevBuf newpool;
+    CU(newpool.ensure((size_t)newcap * ctx->n_pad));
+    if (keep_existing && existing > 0)
+        CU(cudaMemcpyAsync(newpool.p, ctx->pool.p, (size_t)existing * ctx->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->pool.release();
+    ctx->pool = newpool;
+    newpool.p = nullptr;
+    CU(ctx->keys.ensure(slots * 8));
+    CU(ctx->idx.ensure(slots * 4));
+    ctx->table_slots = slots;
+    ctx->pool_cap = newcap;
+    CU(cudaMemsetAsync(ctx->keys.p, 0, slots * 8, ctx->stream));
+    CU(cudaMemsetAsync(ctx->idx.p, 0xFF, slots * 4, ctx->stream));
+    CU(cudaMemsetAsync(counters(ctx) + C_POOL, 0, 8, ctx->stream));
+    if (keep_existing && existing > 0) {
+        // re-insert the existing unique rows into the new table (they stay at the front of the pool)
+        DevBuf tmp;
+        CU(tmp.ensure((size_t)existing * ctx->n_pad));
+        CU(cudaMemcpyAsync(tmp.p, ctx->pool.p, (size_t)existing * ctx->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+        HashSet hs{ctx->keys.as<unsigned long long>(), ctx->idx.as<int32_t>(), slots - 1, ctx->pool.as<int8_t>(),
+                   ctx->pool_cap, counters(ctx) + C_POOL, reinterpret_cast<int*>(counters(ctx) + C_OVF)};
+        CU(launch_dedupe(tmp.as<int8_t>(), existing, ctx->n_pad, ctx->n_pad, hs, ctx->stream));
+        ctx->launches++;
+        CU(cudaStreamSynchronize(ctx->stream));
+        tmp.release();
+    }
+    return MAPLE_OK;
+}
+
+HashSet hashset(maple_ctx* ctx) {
+    return HashSet{ctx->keys.as<unsigned long long>(), ctx->idx.as<int32_t>(), ctx->table_slots - 1,
+                   ctx->pool.as<int8_t>(), ctx->pool_cap, counters(ctx) + C_POOL,
+                   reinterpret_cast<int*>(counters(ctx) + C_OVF)};
+}
+
+// check -> filter -> compact -> lex sort of the ctx pool (pool_count rows) into a new dirset
+int finish_set(maple_ctx* ctx, int64_t pool_count, int filter_minimal, maple_dirset** out) {
+    cudaStream_t s = ctx->stream;
+    const int np = ctx->n_pad;
+    const int64_t K = pool_count;
+    CU(ctx->flags.ensure(std::max<int64_t>(K, 1)));
+    CU(ctx->keep.ensure(std::max<int64_t>(K, 1)));
+    CU(ctx->witness.ensure(std::max<int64_t>(K, 1) * 4));
+    CU(ctx->order.ensure(std::max<int64_t>(K, 1) * 4));
+    CU(ctx->l1.ensure(std::max<int64_t>(K, 1) * 4));
+    CU(ctx->codes.ensure(std::max<int64_t>(K, 1) * 2 * std::max(ctx->Wh, 1) * 4));
+    CU(ctx->hist.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(ctx->level_start.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(ctx->cursor.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(ctx->tmp_rows.ensure(std::max<int64_t>(K, 1) * np));
+    CU(cudaEventRecord(ctx->ev[2], s));
+    CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
+                   ctx->nnz, ctx->dbox.as<int32_t>()};
+    CU(cudaMemsetAsync(counters(ctx) + C_BAD, 0, 16, s));
+    CU(launch_check(ctx->pool.as<int8_t>(), K, cp, ctx->flags.as<uint8_t>(), counters(ctx) + C_BAD, s));
+    if (K > 0) ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[3], s));
+    if (filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->bit_coord.as<int32_t>(), ctx->bit_k.as<int32_t>(),
+                  ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
+                  ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
+                  ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh};
+    int nl = 0;
+    CU(launch_filter(ctx->pool.as<int8_t>(), ctx->flags.as<uint8_t>(), K, fw, filter_minimal, s, &nl));
+    ctx->launches += nl;
+    CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), K, np, ctx->tmp_rows.as<int8_t>(),
+                      counters(ctx) + C_KEEP, s));
+    if (K > 0) ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[4], s));
+    unsigned long long h[C_N];
+    int rc = read_counters(ctx, h);
+    if (rc) return rc;
+    const int64_t M = (int64_t)h[C_KEEP];
+    maple_dirset* ds = new maple_dirset();
+    ds->ctx = ctx;
+    ds->n = ctx->n;
+    ds->n_pad = np;
+    ds->size = M;
+    ds->pool_size = K - (int64_t)h[C_BAD];
+    ds->n_bad = (int64_t)h[C_BAD];
+    cudaError_t e = cudaMalloc(&ds->rows, std::max<int64_t>(M, 1) * np);
+    if (e != cudaSuccess) {
+        delete ds;
+        CU(e);
+    }
+    CU(ctx->sortkeys.ensure(std::max<int64_t>(M, 1) * np));
+    CU(ctx->sidx0.ensure(std::max<int64_t>(M, 1) * 4));
+    CU(ctx->sidx1.ensure(std::max<int64_t>(M, 1) * 4));
+    nl = 0;
+    CU(launch_lex_sort(ctx->tmp_rows.as<int8_t>(), M, ctx->n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
+                       ctx->sidx1.as<int32_t>(), ds->rows, s, &nl));
+    ctx->launches += nl;
+    CU(cudaEventRecord(ctx->ev[5], s));
+    CU(cudaStreamSynchronize(s));
+    *out = ds;
+    return MAPLE_OK;
+}
+
+__global__ void canonical_copy_kernel(const int8_t* __restrict__ rows, int64_t k, int stride, int n, int n_pad,
+                                      int8_t* out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < k; r += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t* g = rows + (size_t)r * stride;
+        int sgn = 0;
+        for (int i = 0; i < n && !sgn; ++i) sgn = g[i] > 0 ? 1 : (g[i] < 0 ? -1 : 0);
+        if (!sgn) sgn = 1;
+        int8_t* o = out + (size_t)r * n_pad;
+        for (int i = 0; i < n_pad; ++i) o[i] = i < n ? (int8_t)(sgn * g[i]) : (int8_t)0;
+    }
+}
+
+int insert_rows_and_finish(maple_ctx* ctx, const int8_t* drows, int64_t k, int stride, int filter_minimal,
+                           maple_dirset** out) {
+    cudaStream_t s = ctx->stream;
+    CU(cudaEventRecord(ctx->ev[0], s));
+    CU(cudaEventRecord(ctx->ev[1], s));
+    CU(ctx->cand.ensure(std::max<int64_t>(k, 1) * ctx->n_pad));
+    if (k > 0) {
+        unsigned blocks = (unsigned)std::min<int64_t>((k + 255) / 256, 148 * 16);
+        canonical_copy_kernel<<<blocks, 256, 0, s>>>(drows, k, stride, ctx->n, ctx->n_pad, ctx->cand.as<int8_t>());
+        CU(cudaGetLastError());
+        ctx->launches++;
+    }
+    int rc = ensure_set(ctx, std::max<int64_t>(k, 1), false, 0);
+    if (rc) return rc;
+    CU(cudaMemsetAsync(counters(ctx) + C_OVF, 0, 8, s));
+    CU(launch_dedupe(ctx->cand.as<int8_t>(), k, ctx->n_pad, ctx->n_pad, hashset(ctx), s));
+    if (k > 0) ctx->launches++;
+    unsigned long long h[C_N];
+    rc = read_counters(ctx, h);
+    if (rc) return rc;
+    if (h[C_OVF]) FAIL(MAPLE_ERR_CAPACITY, "hash set overflow");
+    rc = finish_set(ctx, (int64_t)h[C_POOL], filter_minimal, out);
+    if (rc) return rc;
+    float t;
+    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
+    ctx->t_extract[1] = t;
+    cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]);
+    ctx->t_extract[2] = t;
+    cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
+    ctx->t_extract[3] = t;
+    cudaEventElapsedTime(&t, ctx->ev[4], ctx->ev[5]);
+    ctx->t_extract[4] = t;
+    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[5]);
+    ctx->t_extract[5] = t;
+    ctx->t_extract[0] = 0;
+    return MAPLE_OK;
+}
+
+int build_step_table(maple_ctx* ctx, int T, double lr) {
+    std::vector<float2> tab(T);
+    for (int t = 1; t <= T; ++t) {
+        const double bc1 = 1.0 - std::pow(ctx->beta1, t);
+        const double bc2 = 1.0 - std::pow(ctx->beta2, t);
+        tab[t - 1] = make_float2((float)(lr / bc1), (float)std::sqrt(bc2));
+    }
+    CU(ctx->step_tab.ensure(sizeof(float2) * T));
+    CU(cudaMemcpyAsync(ctx->step_tab.p, tab.data(), sizeof(float2) * T, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MAPLE_OK;
+}
+
+DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_total, int64_t begin, int64_t count) {
+    DescentParams p{};
+    p.n = ctx->n;
+    p.d = ctx->d;
+    p.n_pad = ctx->n_pad;
+    p.T = T;
+    p.lam1 = (float)ctx->lam1;
+    p.lam2 = (float)ctx->lam2;
+    p.beta1 = (float)ctx->beta1;
+    p.beta2 = (float)ctx->beta2;
+    p.eps = (float)ctx->eps;
+    p.step_tab = ctx->step_tab.as<float2>();
+    p.seed = seed;
+    p.n_total = n_total;
+    p.begin = begin;
+    p.count = count;
+    p.B_nd = ctx->B_nd.as<float>();
+    p.B_dn = ctx->B_dn.as<float>();
+    p.B8_nd = ctx->B8.as<int8_t>();
+    p.Bp = ctx->dBp.as<double>();
+    p.lo = ctx->dl.as<int32_t>();
+    p.hi = ctx->du.as<int32_t>();
+    p.box = ctx->dbox.as<int32_t>();
+    return p;
+}
+
+cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
+    const bool tc = ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && descent_tc_supported(ctx->n, ctx->d));
+    ctx->launches++;
+    if (tc) return launch_descent_tc(p, ctx->stream);
+    return launch_descent_simt(p, ctx->stream);
+}
+
+int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps, double lr) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    if (n_starts < 1) FAIL(MAPLE_ERR_BAD_ARG, "n_starts must be >= 1");
+    if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
+    if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
+    if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
+    if (ctx->descent_kernel == 2 && !descent_tc_supported(ctx->n, ctx->d))
+        FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
+    return MAPLE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const int32_t* u, int device,
+                 maple_ctx** out) {
+    maple_ctx* ctx = nullptr;
+    if (!A || !l || !u || !out || m < 1 || n < 1) return MAPLE_ERR_BAD_ARG;
+    *out = nullptr;
+    for (int i = 0; i < n; ++i)
+        if (l[i] > u[i]) return MAPLE_ERR_BAD_BOUNDS;
+    if (m >= n) return MAPLE_ERR_FULL_RANK;
+    if (n > MAPLE_MAX_N) return MAPLE_ERR_RANGE;
+    for (int i = 0; i < n; ++i)
+        if ((int64_t)u[i] - l[i] > 127) return MAPLE_ERR_RANGE;
+    std::unique_ptr<maple_ctx> hold(new maple_ctx());
+    ctx = hold.get();
+    ctx->m = m;
+    ctx->n = n;
+    ctx->d = n - m;
+    ctx->n_pad = round_up(std::max(n, 16), 16);
+    ctx->A.assign(A, A + (size_t)m * n);
+    ctx->l.assign(l, l + n);
+    ctx->u.assign(u, u + n);
+    ctx->box.resize(n);
+    for (int i = 0; i < n; ++i) ctx->box[i] = u[i] - l[i];
+    std::string err;
+    int rc = host_kernel_basis(A, m, n, ctx->B, err);
+    if (rc == 0) rc = host_lll(ctx->B, n, ctx->d, err);
+    if (rc == 0) rc = host_pinv(ctx->B, n, ctx->d, ctx->Bp, err);
+    if (rc) return rc;
+    const int d = ctx->d;
+    // exact re-verification of Thm. 1's A B = 0 and the int8 device range
+    for (int r = 0; r < m; ++r)
+        for (int j = 0; j < d; ++j) {
+            __int128 s = 0;
+            for (int i = 0; i < n; ++i) s += (__int128)A[(size_t)r * n + i] * ctx->B[(size_t)i * d + j];
+            if (s != 0) return MAPLE_ERR_OVERFLOW;
+        }
+    for (int64_t v : ctx->B)
+        if (v > 127 || v < -127) return MAPLE_ERR_RANGE;
+    if (cudaSetDevice(device) != cudaSuccess) return MAPLE_ERR_CUDA;
+    ctx->device = device;
+    for (auto& e : ctx->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return MAPLE_ERR_CUDA;
+    // CSR of A
+    std::vector<int32_t> rp(m + 1, 0), col, val;
+    for (int r = 0; r < m; ++r) {
+        for (int i = 0; i < n; ++i)
+            if (A[(size_t)r * n + i]) {
+                col.push_back(i);
+                val.push_back(A[(size_t)r * n + i]);
+            }
+        rp[r + 1] = (int32_t)col.size();
+    }
+    ctx->nnz = (int)col.size();
+    std::vector<float> bnd((size_t)n * d), bdn((size_t)d * n);
+    std::vector<int8_t> b8((size_t)n * d);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < d; ++j) {
+            const int64_t v = ctx->B[(size_t)i * d + j];
+            bnd[(size_t)i * d + j] = (float)v;
+            bdn[(size_t)j * n + i] = (float)v;
+            b8[(size_t)i * d + j] = (int8_t)v;
+        }
+    // thermometer bit map (filter): P half has Lh = sum(u - l) bits
+    std::vector<int32_t> bc, bk;
+    for (int i = 0; i < n; ++i)
+        for (int k = 1; k <= ctx->box[i]; ++k) {
+            bc.push_back(i);
+            bk.push_back(k);
+        }
+    ctx->Lh = (int)bc.size();
+    ctx->Wh = (ctx->Lh + 31) / 32;
+    CU(upload(ctx->A_rowptr, rp));
+    CU(upload(ctx->A_col, col));
+    CU(upload(ctx->A_val, val));
+    CU(upload(ctx->dl, ctx->l));
+    CU(upload(ctx->du, ctx->u));
+    CU(upload(ctx->dbox, ctx->box));
+    CU(upload(ctx->B_nd, bnd));
+    CU(upload(ctx->B_dn, bdn));
+    CU(upload(ctx->B8, b8));
+    CU(upload(ctx->dBp, ctx->Bp));
+    CU(upload(ctx->bit_coord, bc));
+    CU(upload(ctx->bit_k, bk));
+    CU(ctx->counters.ensure(sizeof(unsigned long long) * C_N));
+    CU(cudaMemset(ctx->counters.p, 0, sizeof(unsigned long long) * C_N));
+    *out = hold.release();
+    return MAPLE_OK;
+}
+
+int maple_kernel_basis(const int32_t* A, int32_t m, int32_t n, int32_t* B_out, double* Bp_out) {
+    if (!A || !B_out || m < 1 || n < 1) return MAPLE_ERR_BAD_ARG;
+    if (m >= n) return MAPLE_ERR_FULL_RANK;
+    std::vector<int64_t> B;
+    std::vector<double> Bp;
+    std::string err;
+    const int d = n - m;
+    int rc = host_kernel_basis(A, m, n, B, err);
+    if (rc == 0) rc = host_lll(B, n, d, err);
+    if (rc == 0 && Bp_out) rc = host_pinv(B, n, d, Bp, err);
+    if (rc) return rc;
+    for (size_t i = 0; i < B.size(); ++i) {
+        if (B[i] > INT32_MAX || B[i] < INT32_MIN) return MAPLE_ERR_OVERFLOW;
+        B_out[i] = (int32_t)B[i];
+    }
+    if (Bp_out) std::memcpy(Bp_out, Bp.data(), Bp.size() * sizeof(double));
+    return MAPLE_OK;
+}
+
+void maple_destroy(maple_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
+                      &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->bit_coord, &ctx->bit_k, &ctx->step_tab, &ctx->cand,
+                      &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
+                      &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
+                      &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
+                      &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,
+                      &ctx->af2b};
+    for (DevBuf* b : bufs) b->release();
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    delete ctx;
+}
+
+int maple_set_stream(maple_ctx* ctx, void* stream) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    ctx->stream = reinterpret_cast<cudaStream_t>(stream);
+    return MAPLE_OK;
+}
+
+int maple_set_extract_params(maple_ctx* ctx, double lambda1, double lambda2, double beta1, double beta2, double eps,
+                             int32_t filter_minimal) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    if (!(lambda1 >= 0) || !(lambda2 >= 0) || !(beta1 >= 0 && beta1 < 1) || !(beta2 >= 0 && beta2 < 1) || !(eps > 0))
+        FAIL(MAPLE_ERR_BAD_ARG, "bad extraction parameters");
+    ctx->lam1 = lambda1;
+    ctx->lam2 = lambda2;
+    ctx->beta1 = beta1;
+    ctx->beta2 = beta2;
+    ctx->eps = eps;
+    ctx->filter_minimal = filter_minimal ? 1 : 0;
+    return MAPLE_OK;
+}
+
+int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
+    if (!ctx || which < 0 || which > 2) return MAPLE_ERR_BAD_ARG;
+    ctx->descent_kernel = which;
+    return MAPLE_OK;
+}
+
+int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    ctx->debug_keep = keep_candidates ? 1 : 0;
+    return MAPLE_OK;
+}
+
+int maple_get_basis(const maple_ctx* ctx, int32_t* B_out) {
+    if (!ctx || !B_out) return MAPLE_ERR_BAD_ARG;
+    for (size_t i = 0; i < ctx->B.size(); ++i) B_out[i] = (int32_t)ctx->B[i];
+    return MAPLE_OK;
+}
+
+int maple_get_pinv(const maple_ctx* ctx, double* Bp_out) {
+    if (!ctx || !Bp_out) return MAPLE_ERR_BAD_ARG;
+    std::memcpy(Bp_out, ctx->Bp.data(), ctx->Bp.size() * sizeof(double));
+    return MAPLE_OK;
+}
+
+int32_t maple_dim_n(const maple_ctx* ctx) { return ctx ? ctx->n : -1; }
+int32_t maple_dim_d(const maple_ctx* ctx) { return ctx ? ctx->d : -1; }
+const char* maple_last_error(const maple_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+int64_t maple_kernel_launches(const maple_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int maple_last_timings(const maple_ctx* ctx, float* e6, float* a3) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    if (e6) std::memcpy(e6, ctx->t_extract, sizeof(ctx->t_extract));
+    if (a3) std::memcpy(a3, ctx->t_augment, sizeof(ctx->t_augment));
+    return MAPLE_OK;
+}
+
+int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
+                        double step_size, uint64_t seed, maple_dirset** out) {
+    int rc = check_extract_args(ctx, n_starts, begin, end, steps, step_size);
+    if (rc) return rc;
+    if (!out) FAIL(MAPLE_ERR_BAD_ARG, "out is null");
+    if (ctx->filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    rc = build_step_table(ctx, steps, step_size);
+    if (rc) return rc;
+    const int np = ctx->n_pad;
+    const int64_t chunk_max = 1 << 18;
+    if (ctx->cand_cap == 0) {
+        const int64_t want = std::min<int64_t>((int64_t)std::max<int64_t>(end - begin, 1) * 8, (int64_t)1 << 22);
+        CU(ctx->cand.ensure((size_t)want * np));
+        ctx->cand_cap = want;
+    }
+    rc = ensure_set(ctx, std::max<int64_t>(ctx->pool_cap, 4096), false, 0);
+    if (rc) return rc;
+    ctx->dbg_cand.clear();
+    ctx->dbg_count = 0;
+    float t_desc = 0.f, t_dd = 0.f;
+    CU(cudaEventRecord(ctx->ev[0], s));
+    int64_t pool_now = 0;
+    for (int64_t c0 = begin; c0 < end;) {
+        const int64_t cnt = std::min(chunk_max, end - c0);
+        unsigned long long h[C_N];
+        for (;;) {
+            CU(cudaMemsetAsync(counters(ctx) + C_CAND, 0, 8, s));
+            DescentParams p = descent_params(ctx, steps, seed, n_starts, c0, cnt);
+            p.harvest = 1;
+            p.cand = ctx->cand.as<int8_t>();
+            p.cand_cap = ctx->cand_cap;
+            p.cand_count = counters(ctx) + C_CAND;
+            CU(cudaEventRecord(ctx->ev[6], s));
+            CU(run_descent(ctx, p));
+            CU(cudaEventRecord(ctx->ev[7], s));
+            rc = read_counters(ctx, h);
+            if (rc) return rc;
+            float t;
+            cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
+            t_desc += t;
+            if ((int64_t)h[C_CAND] <= ctx->cand_cap) break;
+            // the candidate buffer was too small: grow to the exact count and recompute this chunk
+            const int64_t want = (int64_t)h[C_CAND] + ((int64_t)h[C_CAND] >> 3) + 1024;
+            ctx->cand.release();
+            CU(ctx->cand.ensure((size_t)want * np));
+            ctx->cand_cap = want;
+        }
+        const int64_t nc = (int64_t)h[C_CAND];
+        if (ctx->debug_keep && nc > 0) {
+            const size_t off = ctx->dbg_cand.size();
+            ctx->dbg_cand.resize(off + (size_t)nc * np);
+            CU(cudaMemcpy(ctx->dbg_cand.data() + off, ctx->cand.p, (size_t)nc * np, cudaMemcpyDeviceToHost));
+            ctx->dbg_count += nc;
+        }
+        if (pool_now + nc > ctx->pool_cap) {
+            rc = ensure_set(ctx, pool_now + nc, true, pool_now);
+            if (rc) return rc;
+        }
+        CU(cudaEventRecord(ctx->ev[6], s));
+        CU(cudaMemsetAsync(counters(ctx) + C_OVF, 0, 8, s));
+        CU(launch_dedupe(ctx->cand.as<int8_t>(), nc, np, np, hashset(ctx), s));
+        if (nc > 0) ctx->launches++;
+        CU(cudaEventRecord(ctx->ev[7], s));
+        rc = read_counters(ctx, h);
+        if (rc) return rc;
+        float t;
+        cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
+        t_dd += t;
+        if (h[C_OVF]) FAIL(MAPLE_ERR_CAPACITY, "hash set overflow");
+        pool_now = (int64_t)h[C_POOL];
+        c0 += cnt;
+    }
+    CU(cudaEventRecord(ctx->ev[1], s));
+    rc = finish_set(ctx, pool_now, ctx->filter_minimal, out);
+    if (rc) return rc;
+    float t;
+    ctx->t_extract[0] = t_desc;
+    ctx->t_extract[1] = t_dd;
+    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[3]);
+    ctx->t_extract[2] = t;
+    cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
+    ctx->t_extract[3] = t;
+    cudaEventElapsedTime(&t, ctx->ev[4], ctx->ev[5]);
+    ctx->t_extract[4] = t;
+    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[5]);
+    ctx->t_extract[5] = t;
+    return MAPLE_OK;
+}
+
+int maple_extract(maple_ctx* ctx, int64_t n_starts, int32_t steps, double step_size, uint64_t seed,
+                  maple_dirset** out) {
+    return maple_extract_range(ctx, n_starts, 0, n_starts, steps, step_size, seed, out);
+}
+
+int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t stride, maple_dirset** out) {
+    if (!ctx || !out || k < 0 || (k > 0 && !rows) || stride < ctx->n) return MAPLE_ERR_BAD_ARG;
+    if (ctx->filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    CU(cudaSetDevice(ctx->device));
+    return insert_rows_and_finish(ctx, rows, k, stride, ctx->filter_minimal, out);
+}
+
+int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32_t filter_minimal,
+                           maple_dirset** out) {
+    if (!ctx || !out || k < 0 || (k > 0 && !rows)) return MAPLE_ERR_BAD_ARG;
+    if (filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    CU(cudaSetDevice(ctx->device));
+    const int np = ctx->n_pad;
+    std::vector<int8_t> h((size_t)std::max<int64_t>(k, 1) * np, 0);
+    for (int64_t r = 0; r < k; ++r)
+        for (int i = 0; i < ctx->n; ++i) {
+            const int32_t v = rows[(size_t)r * ctx->n + i];
+            if (v > 127 || v < -127) FAIL(MAPLE_ERR_RANGE, "row entry outside int8");
+            h[(size_t)r * np + i] = (int8_t)v;
+        }
+    DevBuf tmp;
+    CU(tmp.ensure(h.size()));
+    CU(cudaMemcpy(tmp.p, h.data(), h.size(), cudaMemcpyHostToDevice));
+    int rc = insert_rows_and_finish(ctx, tmp.as<int8_t>(), k, np, filter_minimal ? 1 : 0, out);
+    tmp.release();
+    return rc;
+}
+
+int64_t maple_dirset_size(const maple_dirset* ds) { return ds ? ds->size : -1; }
+int64_t maple_dirset_pool_size(const maple_dirset* ds) { return ds ? ds->pool_size : -1; }
+int32_t maple_dirset_stride(const maple_dirset* ds) { return ds ? ds->n_pad : -1; }
+const int8_t* maple_dirset_device_rows(const maple_dirset* ds) { return ds ? ds->rows : nullptr; }
+
+int maple_dirset_copy(const maple_dirset* ds, int32_t* host_rows) {
+    if (!ds || (!host_rows && ds->size > 0)) return MAPLE_ERR_BAD_ARG;
+    if (ds->size == 0) return MAPLE_OK;
+    maple_ctx* ctx = ds->ctx;
+    std::vector<int8_t> h((size_t)ds->size * ds->n_pad);
+    CU(cudaMemcpyAsync(h.data(), ds->rows, h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (int64_t r = 0; r < ds->size; ++r)
+        for (int i = 0; i < ds->n; ++i) host_rows[(size_t)r * ds->n + i] = h[(size_t)r * ds->n_pad + i];
+    return MAPLE_OK;
+}
+
+int maple_dirset_copy_device(const maple_dirset* ds, int8_t* dst) {
+    if (!ds || (!dst && ds->size > 0)) return MAPLE_ERR_BAD_ARG;
+    if (ds->size == 0) return MAPLE_OK;
+    maple_ctx* ctx = ds->ctx;
+    CU(cudaMemcpyAsync(dst, ds->rows, (size_t)ds->size * ds->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MAPLE_OK;
+}
+
+void maple_dirset_free(maple_dirset* ds) {
+    if (!ds) return;
+    if (ds->rows) cudaFree(ds->rows);
+    if (ds->D) cudaFree(ds->D);
+    delete ds;
+}
+
+int64_t maple_debug_candidates(maple_ctx* ctx, int32_t* host_rows, int64_t cap) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    if (host_rows) {
+        const int64_t k = std::min(cap, ctx->dbg_count);
+        for (int64_t r = 0; r < k; ++r)
+            for (int i = 0; i < ctx->n; ++i)
+                host_rows[(size_t)r * ctx->n + i] = ctx->dbg_cand[(size_t)r * ctx->n_pad + i];
+    }
+    return ctx->dbg_count;
+}
+
+int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
+                        double step_size, uint64_t seed, float* Z_out, double* Z0_out) {
+    int rc = check_extract_args(ctx, n_starts, begin, end, steps, step_size);
+    if (rc) return rc;
+    if (!Z_out) FAIL(MAPLE_ERR_BAD_ARG, "Z_out is null");
+    CU(cudaSetDevice(ctx->device));
+    rc = build_step_table(ctx, steps, step_size);
+    if (rc) return rc;
+    const int64_t cnt = end - begin;
+    if (cnt == 0) return MAPLE_OK;
+    CU(ctx->zout.ensure((size_t)cnt * ctx->d * sizeof(float)));
+    CU(ctx->z0out.ensure((size_t)cnt * ctx->d * sizeof(double)));
+    DescentParams p = descent_params(ctx, steps, seed, n_starts, begin, cnt);
+    p.harvest = 0;
+    p.Z_out = ctx->zout.as<float>();
+    p.Z0_out = ctx->z0out.as<double>();
+    CU(run_descent(ctx, p));
+    CU(cudaMemcpyAsync(Z_out, ctx->zout.p, (size_t)cnt * ctx->d * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    if (Z0_out)
+        CU(cudaMemcpyAsync(Z0_out, ctx->z0out.p, (size_t)cnt * ctx->d * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MAPLE_OK;
+}
+
+static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, const maple_objective* f,
+                        const int32_t* b, const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best,
+                        int32_t* iters) {
+    const int n = ctx->n, m = ctx->m, np = ctx->n_pad;
+    cudaStream_t s = ctx->stream;
+    // exact feasibility of every incumbent
+    for (int t = 0; t < n_inst; ++t)
+        for (int k = 0; k < k0; ++k) {
+            const int32_t* x = x0 + ((size_t)t * k0 + k) * n;
+            for (int i = 0; i < n; ++i)
+                if (x[i] < ctx->l[i] || x[i] > ctx->u[i]) FAIL(MAPLE_ERR_INFEASIBLE, "x0 outside [l, u]");
+            for (int r = 0; r < m; ++r) {
+                int64_t acc = 0;
+                for (int i = 0; i < n; ++i) acc += (int64_t)ctx->A[(size_t)r * n + i] * x[i];
+                if (acc != b[(size_t)t * m + r]) FAIL(MAPLE_ERR_INFEASIBLE, "x0 violates A x = b");
+            }
+        }
+    for (int t = 0; t < n_inst; ++t)
+        if (!f[t].c || !f[t].Q || (f[t].kind != MAPLE_OBJ_QUADRATIC && f[t].kind != MAPLE_OBJ_SEPARABLE))
+            FAIL(MAPLE_ERR_BAD_ARG, "bad objective");
+    CU(cudaEventRecord(ctx->ev[0], s));
+    maple_dirset* dsm = const_cast<maple_dirset*>(ds);
+    const int64_t K = ds->size;
+    if (!dsm->D && K > 0) {
+        DevBuf un;
+        CU(un.ensure((size_t)2 * K * np));
+        CU(launch_signed_union(ds->rows, K, np, un.as<int8_t>(), s));
+        ctx->launches++;
+        CU(cudaMalloc(&dsm->D, (size_t)2 * K * np));
+        CU(ctx->sortkeys.ensure((size_t)2 * K * np));
+        CU(ctx->sidx0.ensure((size_t)2 * K * 4));
+        CU(ctx->sidx1.ensure((size_t)2 * K * 4));
+        int nl = 0;
+        CU(launch_lex_sort(un.as<int8_t>(), 2 * K, n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
+                           ctx->sidx1.as<int32_t>(), dsm->D, s, &nl));
+        ctx->launches += nl;
+        CU(cudaStreamSynchronize(s));
+        un.release();
+    }
+    // objective data (dense Q per instance)
+    std::vector<double> Q((size_t)n_inst * n * n, 0.0), c((size_t)n_inst * n), c0(n_inst);
+    for (int t = 0; t < n_inst; ++t) {
+        double* Qt = Q.data() + (size_t)t * n * n;
+        if (f[t].kind == MAPLE_OBJ_QUADRATIC)
+            std::memcpy(Qt, f[t].Q, sizeof(double) * n * n);
+        else
+            for (int i = 0; i < n; ++i) Qt[(size_t)i * n + i] = f[t].Q[i];
+        std::memcpy(c.data() + (size_t)t * n, f[t].c, sizeof(double) * n);
+        c0[t] = f[t].c0;
+    }
+    const int64_t ninc = (int64_t)n_inst * k0;
+    CU(ctx->aQ.ensure(Q.size() * 8));
+    CU(ctx->ac.ensure(c.size() * 8));
+    CU(ctx->ac0.ensure(c0.size() * 8));
+    CU(ctx->aqg.ensure((size_t)std::max<int64_t>(2 * K, 1) * n_inst * 8));
+    CU(ctx->aX.ensure((size_t)ninc * n * 4));
+    CU(ctx->aF2.ensure((size_t)ninc * 8));
+    CU(ctx->aIt.ensure((size_t)ninc * 4));
+    CU(ctx->axb.ensure((size_t)n_inst * n * 4));
+    CU(ctx->af2b.ensure((size_t)n_inst * 8));
+    CU(cudaMemcpyAsync(ctx->aQ.p, Q.data(), Q.size() * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->ac.p, c.data(), c.size() * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->ac0.p, c0.data(), c0.size() * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->aX.p, x0, (size_t)ninc * n * 4, cudaMemcpyHostToDevice, s));
+    AugmentParams p{};
+    p.n = n;
+    p.m = m;
+    p.n_pad = np;
+    p.n_dir = (int)K;
+    p.dirs = dsm->D;
+    p.Q = ctx->aQ.as<double>();
+    p.c = ctx->ac.as<double>();
+    p.c0 = ctx->ac0.as<double>();
+    p.qg = ctx->aqg.as<double>();
+    p.lo = ctx->dl.as<int32_t>();
+    p.hi = ctx->du.as<int32_t>();
+    p.X = ctx->aX.as<int32_t>();
+    p.k0 = k0;
+    p.n_inst = n_inst;
+    p.F2 = ctx->aF2.as<double>();
+    p.iters = ctx->aIt.as<int32_t>();
+    p.max_iter = 1 << 20;
+    CU(launch_augment_qg(p, s));
+    ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[1], s));
+    CU(launch_augment(p, s));
+    CU(launch_augment_best(p, ctx->axb.as<int32_t>(), ctx->af2b.as<double>(), s));
+    ctx->launches += 2;
+    CU(cudaEventRecord(ctx->ev[2], s));
+    std::vector<double> f2(n_inst);
+    CU(cudaMemcpyAsync(x_best, ctx->axb.p, (size_t)n_inst * n * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(f2.data(), ctx->af2b.p, (size_t)n_inst * 8, cudaMemcpyDeviceToHost, s));
+    if (iters) CU(cudaMemcpyAsync(iters, ctx->aIt.p, (size_t)ninc * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    for (int t = 0; t < n_inst; ++t) f_best[t] = f2[t] / 2.0;
+    float t;
+    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
+    ctx->t_augment[0] = t;
+    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
+    ctx->t_augment[1] = t;
+    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[2]);
+    ctx->t_augment[2] = t;
+    return MAPLE_OK;
+}
+
+int maple_augment(maple_ctx* ctx, const maple_dirset* ds, const maple_objective* f, const int32_t* b,
+                  const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best, int32_t* status, int32_t* iters) {
+    if (!ctx || !ds || !f || !b || !x_best || !f_best || !status || k0 < 0 || (k0 > 0 && !x0))
+        return MAPLE_ERR_BAD_ARG;
+    if (ds->n != ctx->n) FAIL(MAPLE_ERR_BAD_ARG, "direction set belongs to another n");
+    CU(cudaSetDevice(ctx->device));
+    if (k0 == 0) {
+        *status = MAPLE_STATUS_NO_FEASIBLE;
+        return MAPLE_OK;
+    }
+    *status = MAPLE_STATUS_OK;
+    return augment_impl(ctx, ds, 1, f, b, x0, k0, x_best, f_best, iters);
+}
+
+int maple_augment_many(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, const maple_objective* f,
+                       const int32_t* b, const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best) {
+    if (!ctx || !ds || !f || !b || !x0 || !x_best || !f_best || n_inst < 1 || k0 < 1) return MAPLE_ERR_BAD_ARG;
+    if (ds->n != ctx->n) FAIL(MAPLE_ERR_BAD_ARG, "direction set belongs to another n");
+    CU(cudaSetDevice(ctx->device));
+    return augment_impl(ctx, ds, n_inst, f, b, x0, k0, x_best, f_best, nullptr);
+}
+
+}  // extern "C"

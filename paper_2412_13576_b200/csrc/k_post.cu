@@ -1,0 +1,427 @@
+// North-star post-processing kernels: dedupe (+ sign twins), exact check, ⊑-minimal filter, compaction
+// and lexicographic sort. Rows are canonical int8 vectors (first nonzero > 0) with stride n_pad.
+//
+//  dedupe   open-addressing hash set over the whole row (64-bit key, full-row compare on a key hit):
+//           set semantics of Alg. 3's "𝒢 ∪ {·}"; sign twins were collapsed by canonicalisation.
+//  check    (C1)-(C3) of §4: A g = 0 in exact int64 (A as CSR in shared memory),
+//           g != 0, l - u <= g <= u - l.
+//  filter   (C4) / Def. 1-2: g is dropped iff some other row h has h ⊑ g or h ⊑ -g.
+//           Rows are encoded as thermometer bitsets P = [g_i >= k], N = [g_i <= -k] (k = 1..u_i-l_i), so
+//           h ⊑ g  <=>  P_h ⊆ P_g and N_h ⊆ N_g,   h ⊑ -g  <=>  P_h ⊆ N_g and N_h ⊆ P_g.
+//           Only rows with strictly smaller L1 norm can dominate, so rows are bucketed by L1 (counting
+//           sort) and each g scans the lower buckets tile by tile with block-wide early exit.
+//  sort     bottom-up merge sort of row indices on big-endian biased keys (lexicographic int8 order).
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace maple {
+
+namespace {
+
+__device__ __forceinline__ uint64_t row_hash(const int4* w, int nw) {
+    uint64_t h = 0x243F6A8885A308D3ULL;
+    for (int i = 0; i < nw; ++i) {
+        const int4 v = w[i];
+        const uint64_t a = ((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x;
+        const uint64_t b = ((uint64_t)(uint32_t)v.w << 32) | (uint32_t)v.z;
+        h = mix64(h ^ a);
+        h = mix64(h ^ b);
+    }
+    return h;
+}
+
+__device__ __forceinline__ bool rows_equal(const int4* a, const int4* b, int nw) {
+    for (int i = 0; i < nw; ++i) {
+        const int4 x = a[i], y = b[i];
+        if (x.x != y.x || x.y != y.y || x.z != y.z || x.w != y.w) return false;
+    }
+    return true;
+}
+
+__global__ void dedupe_kernel(const int8_t* __restrict__ rows, int64_t count, int row_stride, int n_pad,
+                              HashSet hs) {
+    const int nw = n_pad / 16;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r * row_stride);
+        const uint64_t h = row_hash(src, nw);
+        const unsigned long long key = (unsigned long long)(h | 1ULL);
+        uint64_t pos = mix64(h ^ 0x9E3779B97F4A7C15ULL) & hs.mask;
+        for (uint64_t probe = 0; probe <= hs.mask; ++probe) {
+            const unsigned long long prev = atomicCAS(&hs.keys[pos], 0ULL, key);
+            if (prev == 0ULL) {  // we own the slot: publish a new unique row
+                const unsigned long long idx = atomicAdd(hs.pool_count, 1ULL);
+                if ((int64_t)idx >= hs.pool_cap) {
+                    atomicExch(hs.overflow, 1);
+                    atomicExch(&hs.idx[pos], -2);
+                    break;
+                }
+                int4* dst = reinterpret_cast<int4*>(hs.pool + (size_t)idx * n_pad);
+                for (int i = 0; i < nw; ++i) dst[i] = src[i];
+                __threadfence();
+                atomicExch(&hs.idx[pos], (int)idx);
+                break;
+            }
+            if (prev == key) {  // same key: wait for publication, then compare the full row
+                int idx;
+                while ((idx = atomicAdd(&hs.idx[pos], 0)) == -1) {
+                }
+                if (idx == -2) break;  // overflowed insert; reported via hs.overflow
+                __threadfence();
+                const int4* other = reinterpret_cast<const int4*>(hs.pool + (size_t)idx * n_pad);
+                if (rows_equal(src, other, nw)) break;  // duplicate
+            }
+            pos = (pos + 1) & hs.mask;
+        }
+    }
+}
+
+__global__ void check_kernel(const int8_t* __restrict__ rows, int64_t count, CheckParams cp, uint8_t* flags,
+                             unsigned long long* n_bad, int smem_ok) {
+    extern __shared__ int32_t sh[];
+    const int32_t* rp = cp.A_rowptr;
+    const int32_t* col = cp.A_col;
+    const int32_t* val = cp.A_val;
+    if (smem_ok) {
+        int32_t* srp = sh;
+        int32_t* scol = sh + cp.m + 1;
+        int32_t* sval = scol + cp.nnz;
+        for (int i = threadIdx.x; i <= cp.m; i += blockDim.x) srp[i] = cp.A_rowptr[i];
+        for (int i = threadIdx.x; i < cp.nnz; i += blockDim.x) {
+            scol[i] = cp.A_col[i];
+            sval[i] = cp.A_val[i];
+        }
+        __syncthreads();
+        rp = srp;
+        col = scol;
+        val = sval;
+    }
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t* g = rows + (size_t)r * cp.n_pad;
+        bool ok = true, nz = false;
+        for (int i = 0; i < cp.n; ++i) {
+            const int v = g[i];
+            nz |= (v != 0);
+            ok &= (abs(v) <= cp.box[i]);
+        }
+        for (int a = 0; a < cp.m && ok; ++a) {
+            long long s = 0;
+            for (int e = rp[a]; e < rp[a + 1]; ++e) s += (long long)val[e] * (long long)g[col[e]];
+            ok &= (s == 0);
+        }
+        ok &= nz;
+        flags[r] = ok ? 1 : 0;
+        if (!ok) atomicAdd(n_bad, 1ULL);
+    }
+}
+
+// ---- filter ----
+__global__ void codes_kernel(const int8_t* __restrict__ rows, const uint8_t* valid, int64_t count, FilterWork fw) {
+    const int W2 = 2 * fw.Wh;
+    const int64_t total = count * W2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / W2;
+        const int w = (int)(t % W2);
+        const bool neg = w >= fw.Wh;
+        const int wb = neg ? w - fw.Wh : w;
+        const int8_t* g = rows + (size_t)r * fw.n_pad;
+        uint32_t word = 0;
+        for (int b = 0; b < 32; ++b) {
+            const int bit = wb * 32 + b;
+            if (bit >= fw.Lh) break;
+            const int v = g[fw.bit_coord[bit]];
+            const int k = fw.bit_k[bit];
+            const bool on = neg ? (v <= -k) : (v >= k);
+            word |= (on ? 1u : 0u) << b;
+        }
+        fw.codes[r * W2 + w] = word;
+        if (w == 0) {
+            int s = 0;
+            for (int i = 0; i < fw.n; ++i) s += abs((int)g[i]);
+            fw.l1[r] = valid[r] ? s : -1;
+        }
+    }
+}
+
+__global__ void hist_kernel(const int32_t* l1, int64_t count, int32_t* hist) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
+        if (l1[r] >= 0) atomicAdd(&hist[l1[r]], 1);
+}
+
+// exclusive scan of hist[0..nb) -> start[0..nb], single block
+__global__ void scan_kernel(const int32_t* hist, int nb, int32_t* start, int32_t* cursor) {
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int i = 0; i < nb; ++i) {
+            start[i] = acc;
+            cursor[i] = acc;
+            acc += hist[i];
+        }
+        start[nb] = acc;
+    }
+}
+
+__global__ void scatter_kernel(const int32_t* l1, int64_t count, int32_t* cursor, int32_t* order) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
+        if (l1[r] >= 0) order[atomicAdd(&cursor[l1[r]], 1)] = (int32_t)r;
+}
+
+constexpr int kFilterThreads = 256;
+constexpr int kTile = 256;
+
+template <int WH>
+__global__ void __launch_bounds__(kFilterThreads)
+dominance_kernel(FilterWork fw, int32_t n_valid) {
+    __shared__ uint32_t tile[kTile * 2 * WH];
+    __shared__ int32_t tile_row[kTile];
+    const int Wh = fw.Wh;
+    const int W2 = 2 * Wh;
+    const int32_t pos = blockIdx.x * kFilterThreads + threadIdx.x;
+    const bool active0 = pos < n_valid;
+    int32_t row = -1, limit = 0;
+    uint32_t P[WH], N[WH];
+    if (active0) {
+        row = fw.order[pos];
+        limit = fw.level_start[fw.l1[row]];  // rows with strictly smaller L1
+#pragma unroll
+        for (int w = 0; w < WH; ++w) {
+            P[w] = w < Wh ? fw.codes[(size_t)row * W2 + w] : 0u;
+            N[w] = w < Wh ? fw.codes[(size_t)row * W2 + Wh + w] : 0u;
+        }
+    }
+    bool done = !active0 || limit == 0;
+    int32_t wit = -1;
+    // block-wide scan limit
+    __shared__ int32_t smax;
+    if (threadIdx.x == 0) smax = 0;
+    __syncthreads();
+    if (active0) atomicMax(&smax, limit);
+    __syncthreads();
+    const int32_t maxlim = smax;
+    for (int32_t t0 = 0; t0 < maxlim; t0 += kTile) {
+        if (!__syncthreads_or(!done)) break;
+        for (int i = threadIdx.x; i < kTile; i += kFilterThreads) {
+            const int32_t q = t0 + i;
+            const int32_t hr = q < maxlim ? fw.order[q] : -1;
+            tile_row[i] = hr;
+            for (int w = 0; w < 2 * WH; ++w) {
+                const int half = w >= WH, ww = half ? w - WH : w;   // smem: P words [0,WH), N words [WH,2WH)
+                tile[i * 2 * WH + w] = (hr >= 0 && ww < Wh) ? fw.codes[(size_t)hr * W2 + half * Wh + ww] : 0u;
+            }
+        }
+        __syncthreads();
+        if (!done) {
+            const int lim = min(kTile, limit - t0);
+            for (int i = 0; i < lim; ++i) {
+                const uint32_t* hc = &tile[i * 2 * WH];
+                uint32_t pos_v = 0, neg_v = 0;
+#pragma unroll
+                for (int w = 0; w < WH; ++w) {
+                    const uint32_t hp = hc[w], hn = hc[WH + w];
+                    pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
+                    neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
+                }
+                if (pos_v == 0u || neg_v == 0u) {
+                    done = true;
+                    wit = tile_row[i];
+                    break;
+                }
+            }
+            if (t0 + kTile >= limit) done = true;
+        }
+        __syncthreads();
+    }
+    if (active0) {
+        fw.keep[row] = (wit < 0) ? 1 : 0;
+        fw.witness[row] = wit;
+    }
+}
+
+__global__ void keep_all_kernel(const uint8_t* valid, int64_t count, uint8_t* keep, int32_t* witness) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        keep[r] = valid[r];
+        witness[r] = -1;
+    }
+}
+
+__global__ void compact_kernel(const int8_t* __restrict__ rows, const uint8_t* sel, int64_t count, int n_pad,
+                               int8_t* out, unsigned long long* n_out) {
+    const int nw = n_pad / 16;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        if (!sel[r]) continue;
+        const unsigned long long o = atomicAdd(n_out, 1ULL);
+        const int4* s = reinterpret_cast<const int4*>(rows + (size_t)r * n_pad);
+        int4* dd = reinterpret_cast<int4*>(out + (size_t)o * n_pad);
+        for (int i = 0; i < nw; ++i) dd[i] = s[i];
+    }
+}
+
+__global__ void sortkey_kernel(const int8_t* __restrict__ rows, int64_t k, int n_pad, uint32_t* keys, int32_t* idx) {
+    const int nk = n_pad / 4;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * nk; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / nk;
+        const int w = (int)(t % nk);
+        const uint8_t* g = reinterpret_cast<const uint8_t*>(rows + (size_t)r * n_pad + 4 * w);
+        keys[t] = ((uint32_t)(g[0] ^ 0x80) << 24) | ((uint32_t)(g[1] ^ 0x80) << 16) |
+                  ((uint32_t)(g[2] ^ 0x80) << 8) | (uint32_t)(g[3] ^ 0x80);
+        if (w == 0) idx[r] = (int32_t)r;
+    }
+}
+
+__device__ __forceinline__ int key_cmp(const uint32_t* a, const uint32_t* b, int nk) {
+    for (int i = 0; i < nk; ++i) {
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    }
+    return 0;
+}
+
+// one merge pass: runs of width w -> 2w
+__global__ void merge_pass_kernel(const uint32_t* keys, int nk, const int32_t* in, int32_t* out, int64_t k, int64_t w) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < k; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pair = p / (2 * w);
+        const int64_t ls = pair * 2 * w;
+        const int64_t rs = min(ls + w, k);
+        const int64_t re = min(ls + 2 * w, k);
+        const int32_t e = in[p];
+        const uint32_t* ke = keys + (size_t)e * nk;
+        int64_t lo, hi, off;
+        if (p < rs) {  // left element: count right elements < e
+            lo = rs;
+            hi = re;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (key_cmp(keys + (size_t)in[mid] * nk, ke, nk) < 0) lo = mid + 1; else hi = mid;
+            }
+            off = (p - ls) + (lo - rs);
+        } else {  // right element: count left elements <= e
+            lo = ls;
+            hi = rs;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (key_cmp(keys + (size_t)in[mid] * nk, ke, nk) <= 0) lo = mid + 1; else hi = mid;
+            }
+            off = (p - rs) + (lo - ls);
+        }
+        out[ls + off] = e;
+    }
+}
+
+__global__ void gather_kernel(const int8_t* __restrict__ rows, const int32_t* idx, int64_t k, int n_pad, int8_t* out) {
+    const int nw = n_pad / 16;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * nw; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = t / nw;
+        const int w = (int)(t % nw);
+        reinterpret_cast<int4*>(out + (size_t)r * n_pad)[w] =
+            reinterpret_cast<const int4*>(rows + (size_t)idx[r] * n_pad)[w];
+    }
+}
+
+__global__ void signed_union_kernel(const int8_t* __restrict__ rows, int64_t k, int n_pad, int8_t* out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * n_pad; t += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t v = rows[t];
+        out[t] = v;
+        out[k * n_pad + t] = (int8_t)(-v);
+    }
+}
+
+inline unsigned grid_for(int64_t work, int threads = 256) {
+    int64_t b = (work + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > 148 * 32) b = 148 * 32;
+    return (unsigned)b;
+}
+
+}  // namespace
+
+cudaError_t launch_dedupe(const int8_t* rows, int64_t count, int row_stride, int n_pad, const HashSet& hs,
+                          cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    dedupe_kernel<<<grid_for(count), 256, 0, s>>>(rows, count, row_stride, n_pad, hs);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& cp, uint8_t* flags,
+                         unsigned long long* n_bad, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    const size_t smem = (size_t)(cp.m + 1 + 2 * cp.nnz) * 4;
+    const int smem_ok = smem <= 160 * 1024;
+    if (smem_ok && smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    check_kernel<<<grid_for(count), 256, smem_ok ? smem : 0, s>>>(rows, count, cp, flags, n_bad, smem_ok);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t count, FilterWork& fw,
+                          int filter_minimal, cudaStream_t s, int* launches) {
+    if (count <= 0) return cudaSuccess;
+    if (!filter_minimal) {
+        keep_all_kernel<<<grid_for(count), 256, 0, s>>>(valid, count, fw.keep, fw.witness);
+        *launches += 1;
+        return cudaGetLastError();
+    }
+    cudaError_t e;
+    codes_kernel<<<grid_for(count * 2 * fw.Wh), 256, 0, s>>>(rows, valid, count, fw);
+    if ((e = cudaMemsetAsync(fw.hist, 0, sizeof(int32_t) * (fw.Lmax + 2), s)) != cudaSuccess) return e;
+    hist_kernel<<<grid_for(count), 256, 0, s>>>(fw.l1, count, fw.hist);
+    scan_kernel<<<1, 32, 0, s>>>(fw.hist, fw.Lmax + 1, fw.level_start, fw.cursor);
+    scatter_kernel<<<grid_for(count), 256, 0, s>>>(fw.l1, count, fw.cursor, fw.order);
+    *launches += 4;
+    // number of valid rows = level_start[Lmax + 1]; read on host to size the grid
+    int32_t n_valid = 0;
+    if ((e = cudaMemcpyAsync(&n_valid, fw.level_start + fw.Lmax + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s)) !=
+        cudaSuccess)
+        return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(fw.keep, 0, count, s)) != cudaSuccess) return e;
+    if (n_valid == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((n_valid + kFilterThreads - 1) / kFilterThreads);
+    if (fw.Wh <= 1) dominance_kernel<1><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
+    else if (fw.Wh <= 2) dominance_kernel<2><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
+    else if (fw.Wh <= 4) dominance_kernel<4><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
+    else if (fw.Wh <= 8) dominance_kernel<8><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
+    else if (fw.Wh <= 16) dominance_kernel<16><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
+    else return cudaErrorInvalidValue;
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t* out, cudaStream_t s) {
+    if (k <= 0) return cudaSuccess;
+    signed_union_kernel<<<grid_for(k * n_pad), 256, 0, s>>>(rows, k, n_pad, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, int64_t count, int n_pad, int8_t* out,
+                           unsigned long long* n_out, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    compact_kernel<<<grid_for(count), 256, 0, s>>>(rows, sel, count, n_pad, out, n_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uint32_t* keys, int32_t* idx0,
+                            int32_t* idx1, int8_t* out, cudaStream_t s, int* launches) {
+    (void)n;
+    if (k <= 0) return cudaSuccess;
+    const int nk = n_pad / 4;
+    sortkey_kernel<<<grid_for(k * nk), 256, 0, s>>>(rows, k, n_pad, keys, idx0);
+    *launches += 1;
+    int32_t* a = idx0;
+    int32_t* b = idx1;
+    for (int64_t w = 1; w < k; w <<= 1) {
+        merge_pass_kernel<<<grid_for(k), 256, 0, s>>>(keys, nk, a, b, k, w);
+        *launches += 1;
+        int32_t* t = a;
+        a = b;
+        b = t;
+    }
+    gather_kernel<<<grid_for(k * (n_pad / 16)), 256, 0, s>>>(rows, a, k, n_pad, out);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace maple

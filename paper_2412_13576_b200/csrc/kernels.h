@@ -1,0 +1,112 @@
+// Launch wrappers of the MAPLE device kernels (host-callable; implemented in k_*.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace maple {
+
+struct DescentParams {
+    int n, d, n_pad, T;
+    float lam1, lam2, beta1, beta2, eps;
+    const float2* step_tab;       // per step t=1..T: (lr / (1 - beta1^t), sqrt(1 - beta2^t)) as fp32
+    uint64_t seed;
+    int64_t n_total;              // RNG key space (global start count)
+    int64_t begin, count;         // global starts [begin, begin + count)
+    const float* B_nd;            // B, n x d row-major (fp32, exact small integers)
+    const float* B_dn;            // B^T, d x n row-major
+    const int8_t* B8_nd;          // B as int8, n x d
+    const double* Bp;             // B+, d x n row-major
+    const int32_t* lo;            // l (n)
+    const int32_t* hi;            // u (n)
+    const int32_t* box;           // u - l (n)
+    int harvest;                  // 0: descent only (debug)
+    int8_t* cand;                 // candidate rows, stride n_pad
+    int64_t cand_cap;
+    unsigned long long* cand_count;
+    float* Z_out;                 // optional: final iterates (count x d)
+    double* Z0_out;               // optional: starts (count x d)
+};
+
+// SIMT descent + harvest (one warp per start). Returns a cudaError_t.
+cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s);
+// tcgen05 descent + harvest (128 starts per CTA, state resident on chip). Returns cudaErrorNotSupported
+// when the shape does not fit the kernel's tile limits.
+cudaError_t launch_descent_tc(const DescentParams& p, cudaStream_t s);
+bool descent_tc_supported(int n, int d);
+
+struct HashSet {
+    unsigned long long* keys;     // 0 = empty
+    int32_t* idx;                 // row index in pool, -1 = not yet published
+    uint64_t mask;                // slots - 1
+    int8_t* pool;                 // unique rows, stride n_pad
+    int64_t pool_cap;
+    unsigned long long* pool_count;
+    int* overflow;
+};
+
+// Insert rows (stride n_pad) into the set; new unique rows are appended to the pool.
+cudaError_t launch_dedupe(const int8_t* rows, int64_t count, int row_stride, int n_pad, const HashSet& hs,
+                          cudaStream_t s);
+
+struct CheckParams {
+    int m, n, n_pad;
+    const int32_t* A_rowptr;      // CSR of A
+    const int32_t* A_col;
+    const int32_t* A_val;
+    int nnz;
+    const int32_t* box;           // u - l
+};
+// flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= box (conditions C1-C3).
+cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& cp, uint8_t* flags,
+                         unsigned long long* n_bad, cudaStream_t s);
+
+struct FilterWork {
+    int n, n_pad;
+    int Lh, Wh;                   // thermometer bits per half, 32-bit words per half
+    const int32_t* bit_coord;     // Lh: coordinate of each thermometer bit
+    const int32_t* bit_k;         // Lh: threshold k >= 1 of each bit
+    uint32_t* codes;              // count x 2Wh
+    int32_t* l1;                  // count
+    int32_t* hist;                // Lmax + 2
+    int32_t* level_start;         // Lmax + 2
+    int32_t* cursor;              // Lmax + 2
+    int32_t* order;               // count
+    uint8_t* keep;                // count
+    int32_t* witness;             // count
+    int Lmax;
+};
+cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t count, FilterWork& fw,
+                          int filter_minimal, cudaStream_t s, int* launches);
+
+// Gather rows with sel[r] != 0 into out (stride n_pad) in an arbitrary order; count to *n_out (device).
+cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, int64_t count, int n_pad, int8_t* out,
+                           unsigned long long* n_out, cudaStream_t s);
+// Lexicographic sort of k rows (stride n_pad, n bytes compared as signed int8). keys/idx scratch:
+// keys: k * n_pad/4 uint32, idx0/idx1: k int32. Result written to out rows.
+cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uint32_t* keys, int32_t* idx0,
+                            int32_t* idx1, int8_t* out, cudaStream_t s, int* launches);
+
+// ---- augmentation ----
+struct AugmentParams {
+    int n, m, n_pad;
+    int n_dir;                    // canonical directions K; D = ±, sorted lexicographically: 2K entries
+    const int8_t* dirs;           // D, 2K x n_pad (lex sorted, both signs)
+    const double* Q;              // n x n (per instance: Q + inst * n * n)
+    const double* c;              // n (per instance)
+    const double* c0;             // per instance
+    const double* qg;             // per instance: g^T Q g for every D entry (2K)
+    const int32_t* lo;
+    const int32_t* hi;
+    int32_t* X;                   // incumbents, (n_inst * k0) x n, updated in place
+    int k0, n_inst;
+    double* F2;                   // per incumbent: final 2 f(x)
+    int32_t* iters;               // per incumbent
+    int max_iter;
+};
+cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s);
+cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s);
+cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s);
+// D = rows ∪ -rows (2k rows, stride n_pad) written to out (unsorted; the caller lex-sorts it)
+cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t* out, cudaStream_t s);
+
+}  // namespace maple

@@ -1,0 +1,235 @@
+// Host exact lattice step of maple_create — Alg. 3 lines 2-3, run once per A.
+//
+//   HNF (Prop. 1): column operations A C = (H | 0), C unimodular, in checked __int128.
+//   B = C[:, m:]            (Thm. 1 setup: Ker_Z(A) = L(B)).
+//   LLL (Alg. 1) with the paper's Siegel test ||B*_{k-1}||^2 > 2 ||B*_k||^2 (Def. P:136-144):
+//     integer basis updates are exact (checked); the Gram-Schmidt data are long double, recomputed from
+//     exact inner products at every visit of k (Schnorr-Euchner style).
+//   B+ = (B^T B)^{-1} B^T (Remark P:321-324): exact Gram matrix, fp64 Cholesky solve.
+// Independent of oracle/lattice.py (which uses Python big integers and a different LLL bookkeeping).
+#include <cmath>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "lattice.h"
+
+namespace maple {
+namespace {
+
+typedef __int128 i128;
+
+struct Overflow {};
+
+inline i128 mul_chk(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_mul_overflow(a, b, &r)) throw Overflow();
+    return r;
+}
+inline i128 add_chk(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_add_overflow(a, b, &r)) throw Overflow();
+    return r;
+}
+inline i128 sub_chk(i128 a, i128 b) {
+    i128 r;
+    if (__builtin_sub_overflow(a, b, &r)) throw Overflow();
+    return r;
+}
+// floor division for i128
+inline i128 fdiv(i128 a, i128 b) {
+    i128 q = a / b, r = a % b;
+    if (r != 0 && ((r < 0) != (b < 0))) --q;
+    return q;
+}
+inline i128 iabs(i128 a) { return a < 0 ? -a : a; }
+
+}  // namespace
+
+int host_kernel_basis(const int32_t* A, int m, int n, std::vector<int64_t>& B, std::string& err) {
+    // M: m x n working copy (row-major), C: n x n (row-major), columns are what we operate on.
+    std::vector<i128> M(size_t(m) * n), C(size_t(n) * n, 0);
+    for (int i = 0; i < m * n; ++i) M[i] = A[i];
+    for (int i = 0; i < n; ++i) C[size_t(i) * n + i] = 1;
+    auto axpy = [&](int j, int p, i128 q) {  // col_j -= q col_p
+        if (q == 0) return;
+        for (int r = 0; r < m; ++r) M[size_t(r) * n + j] = sub_chk(M[size_t(r) * n + j], mul_chk(q, M[size_t(r) * n + p]));
+        for (int r = 0; r < n; ++r) C[size_t(r) * n + j] = sub_chk(C[size_t(r) * n + j], mul_chk(q, C[size_t(r) * n + p]));
+    };
+    auto cswap = [&](int a, int b) {
+        if (a == b) return;
+        for (int r = 0; r < m; ++r) std::swap(M[size_t(r) * n + a], M[size_t(r) * n + b]);
+        for (int r = 0; r < n; ++r) std::swap(C[size_t(r) * n + a], C[size_t(r) * n + b]);
+    };
+    try {
+        for (int i = 0; i < m; ++i) {
+            const i128* row = &M[size_t(i) * n];
+            for (;;) {
+                int p = -1, cnt = 0;
+                for (int j = i; j < n; ++j)
+                    if (row[j] != 0) {
+                        ++cnt;
+                        if (p < 0 || iabs(row[j]) < iabs(row[p])) p = j;
+                    }
+                if (cnt == 0) {
+                    err = "rank(A) < m: row " + std::to_string(i) + " has no pivot";
+                    return -3;
+                }
+                if (cnt == 1) {
+                    cswap(i, p);
+                    break;
+                }
+                for (int j = i; j < n; ++j)
+                    if (j != p && row[j] != 0) axpy(j, p, fdiv(row[j], row[p]));
+            }
+            if (M[size_t(i) * n + i] < 0) {
+                for (int r = 0; r < m; ++r) M[size_t(r) * n + i] = -M[size_t(r) * n + i];
+                for (int r = 0; r < n; ++r) C[size_t(r) * n + i] = -C[size_t(r) * n + i];
+            }
+            for (int j = 0; j < i; ++j) axpy(j, i, fdiv(M[size_t(i) * n + j], M[size_t(i) * n + i]));
+        }
+    } catch (Overflow&) {
+        err = "integer overflow in HNF (checked __int128)";
+        return -5;
+    }
+    const int d = n - m;
+    B.assign(size_t(n) * d, 0);
+    for (int r = 0; r < n; ++r)
+        for (int j = 0; j < d; ++j) {
+            i128 v = C[size_t(r) * n + m + j];
+            if (v > INT64_MAX || v < INT64_MIN) {
+                err = "kernel basis entry exceeds int64";
+                return -5;
+            }
+            B[size_t(r) * d + j] = (int64_t)v;
+        }
+    return 0;
+}
+
+int host_lll(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
+    if (d <= 1) return 0;
+    // columns b_k as contiguous vectors
+    std::vector<std::vector<i128>> b(d, std::vector<i128>(n));
+    for (int r = 0; r < n; ++r)
+        for (int k = 0; k < d; ++k) b[k][r] = Bnd[size_t(r) * d + k];
+    typedef long double ld;
+    std::vector<std::vector<ld>> mu(d, std::vector<ld>(d, 0)), rr(d, std::vector<ld>(d, 0));
+    std::vector<ld> Bs(d, 0);
+    auto dot = [&](int a, int c) {
+        i128 s = 0;
+        for (int r = 0; r < n; ++r) s = add_chk(s, mul_chk(b[a][r], b[c][r]));
+        return (ld)s;
+    };
+    auto gso_row = [&](int k) {
+        for (int j = 0; j < k; ++j) {
+            ld s = dot(k, j);
+            for (int l = 0; l < j; ++l) s -= mu[j][l] * rr[k][l];
+            rr[k][j] = s;
+            mu[k][j] = s / Bs[j];
+        }
+        ld s = dot(k, k);
+        for (int j = 0; j < k; ++j) s -= mu[k][j] * rr[k][j];
+        Bs[k] = s;
+    };
+    try {
+        gso_row(0);
+        if (Bs[0] <= 0) {
+            err = "dependent kernel columns";
+            return -3;
+        }
+        int k = 1;
+        long iters = 0;
+        while (k < d) {
+            if (++iters > 200000000L) {
+                err = "LLL did not terminate";
+                return -5;
+            }
+            // size-reduce b_k against j = k-1 .. 0 (reading #5), repeating until |mu_kj| <= 1/2
+            for (int pass = 0; pass < 64; ++pass) {
+                gso_row(k);
+                bool changed = false;
+                for (int j = k - 1; j >= 0; --j) {
+                    ld q = std::nearbyint(mu[k][j]);
+                    if (std::fabs(mu[k][j]) > 0.5L + 1e-12L && q != 0) {
+                        i128 qi = (i128)(long long)q;
+                        for (int r = 0; r < n; ++r) b[k][r] = sub_chk(b[k][r], mul_chk(qi, b[j][r]));
+                        for (int l = 0; l < j; ++l) mu[k][l] -= q * mu[j][l];
+                        mu[k][j] -= q;
+                        changed = true;
+                    }
+                }
+                if (!changed) break;
+            }
+            if (Bs[k] <= 0) {
+                err = "dependent kernel columns";
+                return -3;
+            }
+            if (Bs[k - 1] > 2.0L * Bs[k] * (1.0L + 1e-12L)) {  // Siegel test (Alg. 1 line 5)
+                std::swap(b[k], b[k - 1]);
+                gso_row(k - 1);
+                k = (k - 1 > 1) ? k - 1 : 1;
+                if (k == 1) gso_row(0);
+            } else {
+                ++k;
+            }
+        }
+    } catch (Overflow&) {
+        err = "integer overflow in LLL (checked __int128)";
+        return -5;
+    }
+    for (int r = 0; r < n; ++r)
+        for (int k = 0; k < d; ++k) {
+            i128 v = b[k][r];
+            if (v > INT64_MAX || v < INT64_MIN) {
+                err = "LLL basis entry exceeds int64";
+                return -5;
+            }
+            Bnd[size_t(r) * d + k] = (int64_t)v;
+        }
+    return 0;
+}
+
+int host_pinv(const std::vector<int64_t>& B, int n, int d, std::vector<double>& Bp, std::string& err) {
+    // G = B^T B exactly, then Cholesky G = L L^T in long double, Bp = G^{-1} B^T.
+    typedef long double ld;
+    std::vector<ld> G(size_t(d) * d);
+    for (int i = 0; i < d; ++i)
+        for (int j = 0; j <= i; ++j) {
+            i128 s = 0;
+            for (int r = 0; r < n; ++r) s += (i128)B[size_t(r) * d + i] * B[size_t(r) * d + j];
+            G[size_t(i) * d + j] = G[size_t(j) * d + i] = (ld)s;
+        }
+    std::vector<ld> L(size_t(d) * d, 0);
+    for (int j = 0; j < d; ++j) {
+        ld s = G[size_t(j) * d + j];
+        for (int k = 0; k < j; ++k) s -= L[size_t(j) * d + k] * L[size_t(j) * d + k];
+        if (s <= 0) {
+            err = "B^T B is not positive definite";
+            return -3;
+        }
+        L[size_t(j) * d + j] = std::sqrt(s);
+        for (int i = j + 1; i < d; ++i) {
+            ld t = G[size_t(i) * d + j];
+            for (int k = 0; k < j; ++k) t -= L[size_t(i) * d + k] * L[size_t(j) * d + k];
+            L[size_t(i) * d + j] = t / L[size_t(j) * d + j];
+        }
+    }
+    Bp.assign(size_t(d) * n, 0.0);
+    std::vector<ld> y(d);
+    for (int c = 0; c < n; ++c) {  // solve G x = B^T e_c = row c of B
+        for (int i = 0; i < d; ++i) {
+            ld t = (ld)B[size_t(c) * d + i];
+            for (int k = 0; k < i; ++k) t -= L[size_t(i) * d + k] * y[k];
+            y[i] = t / L[size_t(i) * d + i];
+        }
+        for (int i = d - 1; i >= 0; --i) {
+            ld t = y[i];
+            for (int k = i + 1; k < d; ++k) t -= L[size_t(k) * d + i] * y[k];
+            y[i] = t / L[size_t(i) * d + i];
+        }
+        for (int i = 0; i < d; ++i) Bp[size_t(i) * n + c] = (double)y[i];
+    }
+    return 0;
+}
+
+}  // namespace maple

@@ -1,0 +1,83 @@
+"""Multi-GPU plumbing for the hot path: one process per GPU, torch.distributed for the one
+real exchange step.
+
+Extraction shards naturally: rank r of W owns global starts [r N / W, (r+1) N / W) (the RNG is keyed by the
+global start index, so the union of the shards' candidates equals the single-GPU candidate set). Each rank
+extracts, checks, dedupes and ⊑-filters locally (a locally non-minimal row is globally non-minimal), then
+ONE all-gather of the padded local rows (NCCL over NVLink on the GPU path) feeds the global merge
+(dedupe + ⊑ filter + lex sort) that every rank runs on the identical union, so every rank ends with the
+identical set. Augmentation incumbents are sharded the same way and the per-rank bests are all-gathered
+(f, x) with the lexicographic tie-break (reading #19).
+
+The functions take the local compute as callables so that the same exchange logic runs with NCCL on the
+GPU (product path: libmaple) and with gloo on CPU tensors in the tests.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, balanced start range of `rank` (global indices)."""
+    return (n_total * rank) // world, (n_total * (rank + 1)) // world
+
+
+def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather a (k_r, stride) int8 tensor of varying k_r across ranks: one all-gather of the counts,
+    one all-gather of the rows padded to max k_r. Returns the concatenated (sum k_r, stride) rows, in rank
+    order, on local.device."""
+    world = dist.get_world_size(group)
+    dev = local.device
+    k = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
+    ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    dist.all_gather(ks, k, group=group)
+    counts = [int(t.item()) for t in ks]
+    kmax = max(max(counts), 1)
+    stride = local.shape[1]
+    pad = torch.zeros((kmax, stride), dtype=local.dtype, device=dev)
+    pad[: local.shape[0]] = local
+    out = torch.empty((world * kmax, stride), dtype=local.dtype, device=dev)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    parts = [out[r * kmax: r * kmax + counts[r]] for r in range(world)]
+    return torch.cat(parts, dim=0) if parts else out[:0]
+
+
+def best_across_ranks(x_best: np.ndarray, f_best: float, device, group=None):
+    """All-gather every rank's (f, x) and return the global best (min f, ties lexicographically smallest x)."""
+    world = dist.get_world_size(group)
+    n = x_best.shape[0]
+    mine = torch.tensor(np.concatenate([[f_best], x_best.astype(np.float64)]), dtype=torch.float64, device=device)
+    allv = [torch.zeros(n + 1, dtype=torch.float64, device=device) for _ in range(world)]
+    dist.all_gather(allv, mine, group=group)
+    rows = [v.cpu().numpy() for v in allv]
+    best = min(rows, key=lambda r: (r[0], tuple(r[1:].tolist())))
+    return best[1:].astype(np.int64), float(best[0])
+
+
+def sharded_extract(ctx, n_total: int, steps: int, lr: float, seed: int, group=None):
+    """Product path (GPU): local maple_extract_range -> NCCL all-gather -> maple_dirset_merge."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a, b = shard_range(n_total, rank, world)
+    local = ctx.extract_range(n_total, a, b, steps, lr, seed)
+    stride = local.stride
+    buf = torch.zeros((max(local.size, 1), stride), dtype=torch.int8, device=f"cuda:{ctx.device}")
+    if local.size:
+        local.copy_device(buf.data_ptr())
+    rows = gather_rows(buf[: local.size], group)
+    torch.cuda.current_stream().synchronize()
+    merged = ctx.merge_device(rows.data_ptr(), rows.shape[0], stride) if rows.shape[0] else \
+        ctx.dirset_from_host(np.zeros((0, ctx.n), np.int32))
+    return merged, local
+
+
+def sharded_augment(ctx, ds, Q, c, c0, b, X0, group=None, kind=0):
+    """Incumbents sharded by rank; local maple_augment; all-gather of the per-rank bests."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a, e = shard_range(len(X0), rank, world)
+    if e > a:
+        xb, fb, _, _ = ctx.augment(ds, Q, c, c0, b, X0[a:e], kind=kind)
+    else:
+        xb, fb = np.zeros(ctx.n, np.int64), float("inf")
+    return best_across_ranks(np.asarray(xb), fb, f"cuda:{ctx.device}", group)

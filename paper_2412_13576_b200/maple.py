@@ -1,0 +1,303 @@
+"""Thin Python binding of libmaple.so (include/maple.h): argument marshalling only.
+
+Every step of the hot path runs in the library's CUDA kernels; this module converts numpy / torch buffers
+to pointers and back, and raises MapleError on a nonzero status. There is no CPU fallback: if the shared
+library (or a CUDA device) is missing, load() raises.
+
+Low-level functions keep the C names (maple_create, maple_extract, ...); `Context` / `DirSet` wrap them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmaple.so")
+_lib = None
+
+ERRORS = {
+    -1: "BAD_ARG", -2: "BAD_BOUNDS", -3: "RANK_DEFICIENT", -4: "FULL_RANK", -5: "OVERFLOW", -6: "RANGE",
+    -7: "CUDA", -8: "OOM", -9: "CAPACITY", -10: "INFEASIBLE", -11: "COMM",
+}
+OBJ_QUADRATIC, OBJ_SEPARABLE = 0, 1
+STATUS_OK, STATUS_NO_FEASIBLE = 0, 1
+
+class maple_objective(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("Q", C.POINTER(C.c_double)), ("c", C.POINTER(C.c_double)), ("c0", C.c_double)]
+
+
+# (name, restype, argtypes) for every exported symbol of include/maple.h
+_P = C.c_void_p
+_SIGS = [
+    ("maple_create", C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, C.c_int, C.POINTER(_P)]),
+    ("maple_destroy", None, [_P]),
+    ("maple_kernel_basis", C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    ("maple_set_stream", C.c_int, [_P, _P]),
+    ("maple_set_extract_params", C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]),
+    ("maple_get_basis", C.c_int, [_P, _P]),
+    ("maple_get_pinv", C.c_int, [_P, _P]),
+    ("maple_dim_n", C.c_int32, [_P]),
+    ("maple_dim_d", C.c_int32, [_P]),
+    ("maple_last_error", C.c_char_p, [_P]),
+    ("maple_extract", C.c_int, [_P, C.c_int64, C.c_int32, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    ("maple_extract_range", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_uint64,
+                                      C.POINTER(_P)]),
+    ("maple_dirset_merge", C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(_P)]),
+    ("maple_dirset_size", C.c_int64, [_P]),
+    ("maple_dirset_pool_size", C.c_int64, [_P]),
+    ("maple_dirset_copy", C.c_int, [_P, _P]),
+    ("maple_dirset_device_rows", _P, [_P]),
+    ("maple_dirset_stride", C.c_int32, [_P]),
+    ("maple_dirset_copy_device", C.c_int, [_P, _P]),
+    ("maple_dirset_free", None, [_P]),
+    ("maple_dirset_from_host", C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(_P)]),
+    ("maple_augment", C.c_int, [_P, _P, C.POINTER(maple_objective), _P, _P, C.c_int32, _P, _P, _P, _P]),
+    ("maple_augment_many", C.c_int, [_P, _P, C.c_int32, C.POINTER(maple_objective), _P, _P, C.c_int32, _P, _P]),
+    ("maple_debug_descent", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_uint64, _P, _P]),
+    ("maple_set_debug", C.c_int, [_P, C.c_int32]),
+    ("maple_debug_candidates", C.c_int64, [_P, _P, C.c_int64]),
+    ("maple_last_timings", C.c_int, [_P, _P, _P]),
+    ("maple_kernel_launches", C.c_int64, [_P]),
+    ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
+]
+
+
+class MapleError(RuntimeError):
+    def __init__(self, code, msg=""):
+        super().__init__(f"MAPLE_ERR_{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.name = ERRORS.get(code, str(code))
+
+
+def load(path: str = LIB_PATH):
+    """Load libmaple.so (no fallback: raises if it is missing or lacks a symbol)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built; run __graft_entry__.build() (there is no CPU fallback)")
+    lib = C.CDLL(path)
+    for name, res, args in _SIGS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def exported_symbols():
+    return [s[0] for s in _SIGS]
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+def _check(rc, ctx=None):
+    if rc != 0:
+        msg = _lib.maple_last_error(ctx).decode() if ctx else ""
+        raise MapleError(rc, msg)
+
+
+def maple_kernel_basis(A):
+    """Host-only lattice step of maple_create: returns (B, B+) as computed by the library."""
+    load()
+    A = np.ascontiguousarray(A, dtype=np.int32)
+    m, n = A.shape
+    B = np.zeros((n, n - m), np.int32)
+    Bp = np.zeros((n - m, n), np.float64)
+    rc = _lib.maple_kernel_basis(_ptr(A), m, n, _ptr(B), _ptr(Bp))
+    if rc != 0:
+        raise MapleError(rc, "maple_kernel_basis")
+    return B, Bp
+
+
+class DirSet:
+    """A device-resident direction set (canonical rows, lexicographically sorted)."""
+
+    def __init__(self, ctx: "Context", handle):
+        self.ctx = ctx
+        self.h = handle
+
+    @property
+    def size(self) -> int:
+        return int(_lib.maple_dirset_size(self.h))
+
+    @property
+    def pool_size(self) -> int:
+        return int(_lib.maple_dirset_pool_size(self.h))
+
+    @property
+    def stride(self) -> int:
+        return int(_lib.maple_dirset_stride(self.h))
+
+    @property
+    def device_ptr(self) -> int:
+        return _lib.maple_dirset_device_rows(self.h) or 0
+
+    def rows(self) -> np.ndarray:
+        out = np.zeros((self.size, self.ctx.n), dtype=np.int32)
+        _check(_lib.maple_dirset_copy(self.h, _ptr(out) if out.size else None), self.ctx.h)
+        return out
+
+    def copy_device(self, dst_ptr: int):
+        """Copy the rows (size x stride int8) into device memory at dst_ptr."""
+        _check(_lib.maple_dirset_copy_device(self.h, C.c_void_p(dst_ptr)), self.ctx.h)
+
+    def free(self):
+        if self.h:
+            _lib.maple_dirset_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Context:
+    """maple_create(A, l, u): host-exact HNF + LLL + B+ and device upload."""
+
+    def __init__(self, A, l, u, device: int = 0):
+        load()
+        A = np.ascontiguousarray(A, dtype=np.int32)
+        l = np.ascontiguousarray(l, dtype=np.int32)
+        u = np.ascontiguousarray(u, dtype=np.int32)
+        self.m, self.n = A.shape
+        h = C.c_void_p()
+        rc = _lib.maple_create(_ptr(A), self.m, self.n, _ptr(l), _ptr(u), device, C.byref(h))
+        if rc != 0:
+            raise MapleError(rc, "maple_create")
+        self.h = h
+        self.d = int(_lib.maple_dim_d(h))
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.maple_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- configuration ----
+    def set_stream(self, stream_handle: int):
+        _check(_lib.maple_set_stream(self.h, C.c_void_p(stream_handle)), self.h)
+
+    def set_params(self, lambda1=0.85, lambda2=1.0, beta1=0.9, beta2=0.999, eps=1e-8, filter_minimal=True):
+        _check(_lib.maple_set_extract_params(self.h, lambda1, lambda2, beta1, beta2, eps, int(filter_minimal)), self.h)
+
+    def set_descent_kernel(self, which: int):
+        _check(_lib.maple_set_descent_kernel(self.h, which), self.h)
+
+    def set_debug(self, keep_candidates: bool):
+        _check(_lib.maple_set_debug(self.h, int(keep_candidates)), self.h)
+
+    @property
+    def B(self) -> np.ndarray:
+        out = np.zeros((self.n, self.d), dtype=np.int32)
+        _check(_lib.maple_get_basis(self.h, _ptr(out)), self.h)
+        return out
+
+    @property
+    def Bp(self) -> np.ndarray:
+        out = np.zeros((self.d, self.n), dtype=np.float64)
+        _check(_lib.maple_get_pinv(self.h, _ptr(out)), self.h)
+        return out
+
+    # ---- extraction ----
+    def extract(self, n_starts, steps, step_size, seed) -> DirSet:
+        h = C.c_void_p()
+        _check(_lib.maple_extract(self.h, int(n_starts), int(steps), float(step_size), int(seed), C.byref(h)), self.h)
+        return DirSet(self, h)
+
+    def extract_range(self, n_starts, begin, end, steps, step_size, seed) -> DirSet:
+        h = C.c_void_p()
+        _check(_lib.maple_extract_range(self.h, int(n_starts), int(begin), int(end), int(steps), float(step_size),
+                                        int(seed), C.byref(h)), self.h)
+        return DirSet(self, h)
+
+    def merge_device(self, ptr: int, k: int, stride: int) -> DirSet:
+        h = C.c_void_p()
+        _check(_lib.maple_dirset_merge(self.h, C.c_void_p(ptr), int(k), int(stride), C.byref(h)), self.h)
+        return DirSet(self, h)
+
+    def dirset_from_host(self, rows, filter_minimal=True) -> DirSet:
+        rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int32).reshape(-1, self.n))
+        h = C.c_void_p()
+        _check(_lib.maple_dirset_from_host(self.h, _ptr(rows) if rows.size else None, rows.shape[0],
+                                           int(filter_minimal), C.byref(h)), self.h)
+        return DirSet(self, h)
+
+    def debug_descent(self, n_starts, begin, end, steps, step_size, seed):
+        Z = np.zeros((end - begin, self.d), dtype=np.float32)
+        Z0 = np.zeros((end - begin, self.d), dtype=np.float64)
+        _check(_lib.maple_debug_descent(self.h, int(n_starts), int(begin), int(end), int(steps), float(step_size),
+                                        int(seed), _ptr(Z), _ptr(Z0)), self.h)
+        return Z, Z0
+
+    def candidates(self) -> np.ndarray:
+        k = int(_lib.maple_debug_candidates(self.h, None, 0))
+        out = np.zeros((k, self.n), dtype=np.int32)
+        if k:
+            _lib.maple_debug_candidates(self.h, _ptr(out), k)
+        return out
+
+    def timings(self):
+        e = np.zeros(6, np.float32)
+        a = np.zeros(3, np.float32)
+        _check(_lib.maple_last_timings(self.h, _ptr(e), _ptr(a)), self.h)
+        return {"descent": float(e[0]), "dedupe": float(e[1]), "check": float(e[2]), "filter": float(e[3]),
+                "sort": float(e[4]), "extract_total": float(e[5]), "aug_precompute": float(a[0]),
+                "aug_iterate": float(a[1]), "augment_total": float(a[2])}
+
+    def launches(self) -> int:
+        return int(_lib.maple_kernel_launches(self.h))
+
+    # ---- augmentation ----
+    @staticmethod
+    def _objective(Q, c, c0, kind):
+        Q = np.ascontiguousarray(Q, dtype=np.float64)
+        c = np.ascontiguousarray(c, dtype=np.float64)
+        ob = maple_objective(kind, Q.ctypes.data_as(C.POINTER(C.c_double)), c.ctypes.data_as(C.POINTER(C.c_double)),
+                             float(c0))
+        return ob, (Q, c)
+
+    def augment(self, ds: DirSet, Q, c, c0, b, x0, kind=OBJ_QUADRATIC):
+        """maple_augment: returns (x_best, f_best, status, iters per incumbent)."""
+        ob, keep = self._objective(Q, c, c0, kind)
+        b = np.ascontiguousarray(b, dtype=np.int32)
+        x0 = np.ascontiguousarray(np.asarray(x0, dtype=np.int32).reshape(-1, self.n))
+        k0 = x0.shape[0]
+        xb = np.zeros(self.n, np.int32)
+        fb = np.zeros(1, np.float64)
+        st = np.zeros(1, np.int32)
+        it = np.zeros(max(k0, 1), np.int32)
+        _check(_lib.maple_augment(self.h, ds.h, C.byref(ob), _ptr(b), _ptr(x0) if k0 else None, k0, _ptr(xb), _ptr(fb),
+                                  _ptr(st), _ptr(it)), self.h)
+        del keep
+        return xb, float(fb[0]), int(st[0]), it[:k0]
+
+    def augment_many(self, ds: DirSet, Qs, cs, c0s, bs, X0s, kind=OBJ_QUADRATIC):
+        """maple_augment_many over n_inst instances sharing A and the direction set (configs[3])."""
+        n_inst = len(Qs)
+        obs = (maple_objective * n_inst)()
+        keep = []
+        for t in range(n_inst):
+            ob, k = self._objective(Qs[t], cs[t], c0s[t], kind)
+            obs[t] = ob
+            keep.append(k)
+        b = np.ascontiguousarray(np.asarray(bs, dtype=np.int32).reshape(n_inst, self.m))
+        X0 = np.ascontiguousarray(np.asarray(X0s, dtype=np.int32).reshape(n_inst, -1, self.n))
+        k0 = X0.shape[1]
+        xb = np.zeros((n_inst, self.n), np.int32)
+        fb = np.zeros(n_inst, np.float64)
+        _check(_lib.maple_augment_many(self.h, ds.h, n_inst, obs, _ptr(b), _ptr(X0), k0, _ptr(xb), _ptr(fb)), self.h)
+        del keep
+        return xb, fb

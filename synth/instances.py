@@ -129,9 +129,9 @@ def c2b() -> Instance:
     return _finish("C2b", A, np.zeros(n), u, x, Q, c, mv, n_starts=65536, steps=200, lr=0.01, seed=2)
 
 
-def _identity_block(name, m, n, vals, p, seed, **kw) -> Instance:
+def _identity_block(name, m, n, vals, p, gen_seed, **kw) -> Instance:
     """A = [I_m | W] Pi (columns permuted), W_ij in vals with probability p, binary box, b = A x_plant."""
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(gen_seed)
     d = n - m
     mask = rng.random((m, d)) < p
     W = np.where(mask, rng.choice(np.asarray(vals), size=(m, d)), 0)

@@ -1,0 +1,100 @@
+"""CPU tests of the boundary: libmaple.so loads, exports every symbol include/maple.h declares, and its
+host-only lattice step (maple_kernel_basis = the host part of maple_create) is checked against the
+oracle's independent exact checkers (Thm. 1 saturation, Def. 'reduced basis', pseudoinverse)."""
+import re
+import os
+
+import numpy as np
+import pytest
+
+from oracle import lattice as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def maple():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2412_13576_b200 import maple as M
+    M.load()
+    return M
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "maple.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(maple_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_all_exported(maple):
+    import ctypes
+    lib = ctypes.CDLL(maple.LIB_PATH)
+    syms = _header_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert sorted(maple.exported_symbols()) == syms
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    from paper_2412_13576_b200 import maple as M
+    saved = M._lib
+    M._lib = None
+    try:
+        with pytest.raises(ImportError):
+            M.load(str(tmp_path / "missing.so"))
+    finally:
+        M._lib = saved
+
+
+@pytest.mark.parametrize("name", ["C1", "C2a", "C2b"])
+def test_library_basis_is_reduced_kernel_basis(maple, name):
+    from synth import config
+    inst = config(name)
+    B, Bp = maple.maple_kernel_basis(inst.A)
+    assert L.is_kernel_basis(inst.A, B.tolist())          # A B = 0 and L(B) = Ker_Z(A) (Thm. 1)
+    assert L.is_lll_reduced(B.tolist())                   # Def. P:136-144, exact rationals
+    np.testing.assert_allclose(Bp, L.pinv(B), rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("seed", range(25))
+def test_library_basis_random(maple, seed):
+    rng = np.random.default_rng(900 + seed)
+    m = int(rng.integers(1, 5))
+    n = int(rng.integers(m + 1, 10))
+    while True:
+        A = rng.integers(-6, 7, size=(m, n))
+        if np.linalg.matrix_rank(A.astype(float)) == m:
+            break
+    try:
+        B, Bp = maple.maple_kernel_basis(A)
+    except maple.MapleError as e:      # entries beyond the device int8 range are reported, never wrapped
+        assert e.name in ("RANGE", "OVERFLOW")
+        return
+    assert L.is_kernel_basis(A, B.tolist())
+    assert L.is_lll_reduced(B.tolist())
+
+
+def test_library_basis_c3_shape(maple):
+    from synth import c3
+    inst = c3()
+    B, _ = maple.maple_kernel_basis(inst.A)
+    assert B.shape == (300, 280)
+    assert np.all(inst.A @ B == 0)
+    # fp64 reducedness check with tolerance, d = 280
+    Bf = B.astype(np.float64)
+    Qm, R = np.linalg.qr(Bf)
+    diag = np.abs(np.diag(R))
+    mu = R / np.where(diag == 0, 1, diag)[:, None]
+    assert np.all(np.abs(np.triu(mu, 1)) <= 0.5 + 1e-9)
+    assert np.all(diag[:-1] ** 2 <= 2 * diag[1:] ** 2 * (1 + 1e-9))
+
+
+def test_create_errors(maple):
+    with pytest.raises(maple.MapleError) as e:
+        maple.maple_kernel_basis(np.eye(2, dtype=np.int32))
+    assert e.value.name == "FULL_RANK"
+    with pytest.raises(maple.MapleError) as e:
+        maple.maple_kernel_basis(np.array([[1, 2, 3], [2, 4, 6]]))
+    assert e.value.name == "RANK_DEFICIENT"
