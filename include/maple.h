@@ -173,6 +173,11 @@ int64_t maple_debug_candidates(maple_ctx* ctx, int32_t* host_rows, int64_t cap);
 int maple_last_timings(const maple_ctx* ctx, float* extract_ms6, float* augment_ms3);
 /* Number of CUDA kernel launches the library issued since the context was created. */
 int64_t maple_kernel_launches(const maple_ctx* ctx);
+/* tcgen05 self-test on `device` (host buffers): D1 (128x64) = A1 (128x48) B1^T (B1 64x48) with kind::tf32 and
+ * D2 (128x48) = A2 (128x64) B2^T (B2 48x64) with kind::f16, through the same shared-memory layout and
+ * descriptors as the descent kernel; the caller compares with an exact host product. */
+int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1, const float* A2, const float* B2,
+                        float* D2);
 /* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05. */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
 

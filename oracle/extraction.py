@@ -115,22 +115,25 @@ def harvest(Z, B, l, u):
 def descend(z0, B, steps, lr, lam1=0.85, lam2=1.0, beta1=0.9, beta2=0.999, eps=1e-8, dtype=np.float64,
             l=None, u=None, pool=None, trace=None):
     """Alg. 3 lines 6-11 for a batch of starts. Returns the final iterates Z (dtype). If l, u and `pool`
-    (a set) are given, every step's harvest is added to the pool as canonical int tuples."""
+    (a set) are given, every step's harvest is added to the pool as canonical int tuples.
+
+    Scalars follow torch.optim.Adam (reading #9; PyTorch 2.1.0): beta, 1 - beta, the step size
+    lr / (1 - beta1^t) and sqrt(1 - beta2^t) are computed in Python double and then used in `dtype`
+    arithmetic (so the fp32 mode is PyTorch's fp32 Adam; in fp64 mode this is exact)."""
     dt = np.dtype(dtype)
     Z = np.asarray(z0).astype(dt)
     Bd = np.asarray(B, dtype=np.float64)
     m = np.zeros_like(Z)
     v = np.zeros_like(Z)
     b1, b2 = dt.type(beta1), dt.type(beta2)
-    one = dt.type(1)
+    omb1, omb2 = dt.type(1.0 - beta1), dt.type(1.0 - beta2)
     for t in range(1, steps + 1):
         G = subgrad(Z, Bd, lam1, lam2)
-        m = b1 * m + (one - b1) * G
-        v = b2 * v + (one - b2) * G * G
-        bc1 = one - b1 ** t
-        bc2 = one - b2 ** t
-        step = dt.type(lr) / bc1
-        denom = np.sqrt(v) / np.sqrt(bc2) + dt.type(eps)
+        m = b1 * m + omb1 * G
+        v = b2 * v + omb2 * G * G
+        step = dt.type(lr / (1.0 - beta1 ** t))
+        bc2s = dt.type(np.sqrt(1.0 - beta2 ** t))
+        denom = np.sqrt(v) / bc2s + dt.type(eps)
         Z = Z - step * m / denom
         if trace is not None:
             trace.append(Z.copy())

@@ -60,6 +60,7 @@ struct maple_ctx {
     // device constants
     DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, bit_coord, bit_k;
     int nnz = 0, Lh = 0, Wh = 0;
+    double rbound = 0;            // max_j sum_i |B+_ji| (u_i - l_i): bound on |round(z)| of any in-box g
     // params (Eq. 3 / Adam)
     double lam1 = 0.85, lam2 = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
     int filter_minimal = 1;
@@ -310,6 +311,8 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.beta1 = (float)ctx->beta1;
     p.beta2 = (float)ctx->beta2;
     p.eps = (float)ctx->eps;
+    p.omb1 = (float)(1.0 - ctx->beta1);
+    p.omb2 = (float)(1.0 - ctx->beta2);
     p.step_tab = ctx->step_tab.as<float2>();
     p.seed = seed;
     p.n_total = n_total;
@@ -326,7 +329,8 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
 }
 
 cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
-    const bool tc = ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && descent_tc_supported(ctx->n, ctx->d));
+    const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2048.0;
+    const bool tc = ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && tc_ok);
     ctx->launches++;
     if (tc) return launch_descent_tc(p, ctx->stream);
     return launch_descent_simt(p, ctx->stream);
@@ -338,7 +342,7 @@ int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t 
     if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
     if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
     if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
-    if (ctx->descent_kernel == 2 && !descent_tc_supported(ctx->n, ctx->d))
+    if (ctx->descent_kernel == 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2048.0))
         FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
     return MAPLE_OK;
 }
@@ -384,6 +388,11 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         }
     for (int64_t v : ctx->B)
         if (v > 127 || v < -127) return MAPLE_ERR_RANGE;
+    for (int j = 0; j < d; ++j) {
+        double s = 0;
+        for (int i = 0; i < n; ++i) s += std::fabs(ctx->Bp[(size_t)j * n + i]) * ctx->box[i];
+        ctx->rbound = std::max(ctx->rbound, s);
+    }
     if (cudaSetDevice(device) != cudaSuccess) return MAPLE_ERR_CUDA;
     ctx->device = device;
     for (auto& e : ctx->ev)
@@ -488,6 +497,27 @@ int maple_set_extract_params(maple_ctx* ctx, double lambda1, double lambda2, dou
     ctx->beta2 = beta2;
     ctx->eps = eps;
     ctx->filter_minimal = filter_minimal ? 1 : 0;
+    return MAPLE_OK;
+}
+
+int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1, const float* A2, const float* B2,
+                        float* D2) {
+    maple_ctx* ctx = nullptr;
+    if (!A1 || !B1 || !D1 || !A2 || !B2 || !D2) return MAPLE_ERR_BAD_ARG;
+    CU(cudaSetDevice(device));
+    const size_t sz[6] = {128 * 48, 64 * 48, 128 * 64, 128 * 64, 48 * 64, 128 * 48};
+    DevBuf b[6];
+    for (int i = 0; i < 6; ++i) CU(b[i].ensure(sz[i] * 4));
+    CU(cudaMemcpy(b[0].p, A1, sz[0] * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[1].p, B1, sz[1] * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[3].p, A2, sz[3] * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[4].p, B2, sz[4] * 4, cudaMemcpyHostToDevice));
+    CU(umma_selftest(b[0].as<float>(), b[1].as<float>(), b[2].as<float>(), b[3].as<float>(), b[4].as<float>(),
+                     b[5].as<float>(), 0));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(D1, b[2].p, sz[2] * 4, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(D2, b[5].p, sz[5] * 4, cudaMemcpyDeviceToHost));
+    for (auto& x : b) x.release();
     return MAPLE_OK;
 }
 

@@ -66,7 +66,7 @@ descent_simt_kernel(const DescentParams p) {
     }
     __syncwarp();
 
-    const float b1 = p.beta1, b2 = p.beta2, omb1 = 1.f - p.beta1, omb2 = 1.f - p.beta2;
+    const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2;
     for (int t = 0; t < p.T; ++t) {
         // forward: y_i = sum_j B_ij z_j, s_i = sign(y_i)
         for (int i = lane; i < n; i += 32) {

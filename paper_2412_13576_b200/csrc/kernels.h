@@ -8,6 +8,7 @@ namespace maple {
 struct DescentParams {
     int n, d, n_pad, T;
     float lam1, lam2, beta1, beta2, eps;
+    float omb1, omb2;             // (1 - beta1), (1 - beta2) rounded from fp64 (torch.optim.Adam scalars)
     const float2* step_tab;       // per step t=1..T: (lr / (1 - beta1^t), sqrt(1 - beta2^t)) as fp32
     uint64_t seed;
     int64_t n_total;              // RNG key space (global start count)
@@ -33,6 +34,9 @@ cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s);
 // when the shape does not fit the kernel's tile limits.
 cudaError_t launch_descent_tc(const DescentParams& p, cudaStream_t s);
 bool descent_tc_supported(int n, int d);
+// single-tile tcgen05 self-test (device pointers): D1 = A1 B1^T (tf32, 128x48 * 48x64), D2 = A2 B2^T (f16, 128x64 * 64x48)
+cudaError_t umma_selftest(const float* A1, const float* B1, float* D1, const float* A2, const float* B2, float* D2,
+                          cudaStream_t s);
 
 struct HashSet {
     unsigned long long* keys;     // 0 = empty

@@ -61,6 +61,7 @@ _SIGS = [
     ("maple_last_timings", C.c_int, [_P, _P, _P]),
     ("maple_kernel_launches", C.c_int64, [_P]),
     ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
+    ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
 ]
 
 
@@ -112,6 +113,18 @@ def maple_kernel_basis(A):
     if rc != 0:
         raise MapleError(rc, "maple_kernel_basis")
     return B, Bp
+
+
+def maple_selftest_umma(A1, B1, A2, B2, device=0):
+    """Single-tile tcgen05 products D1 = A1 B1^T (tf32) and D2 = A2 B2^T (f16) computed on the device."""
+    load()
+    A1, B1, A2, B2 = (np.ascontiguousarray(x, dtype=np.float32) for x in (A1, B1, A2, B2))
+    D1 = np.zeros((128, 64), np.float32)
+    D2 = np.zeros((128, 48), np.float32)
+    rc = _lib.maple_selftest_umma(device, _ptr(A1), _ptr(B1), _ptr(D1), _ptr(A2), _ptr(B2), _ptr(D2))
+    if rc != 0:
+        raise MapleError(rc, "maple_selftest_umma")
+    return D1, D2
 
 
 class DirSet:

@@ -16,8 +16,13 @@ from oracle import postprocess as OP
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(maple, inst):
-    return maple.Context(inst.A, inst.l, inst.u, device=0)
+SIMT, TC = 1, 2
+
+
+def _ctx(maple, inst, kernel=0):
+    ctx = maple.Context(inst.A, inst.l, inst.u, device=0)
+    ctx.set_descent_kernel(kernel)
+    return ctx
 
 
 def _set(rows):
@@ -45,11 +50,12 @@ def test_basis_and_starts_match_oracle(gpu_lib, name):
     np.testing.assert_allclose(Z0, z0, rtol=1e-12, atol=1e-12)     # fp64 on both sides
 
 
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,T", [("C1", 1), ("C1", 5), ("C2a", 1), ("C2a", 5), ("C2b", 5)])
-def test_descent_iterates_small_T_all_starts(gpu_lib, name, T):
+def test_descent_iterates_small_T_all_starts(gpu_lib, name, T, kernel):
     from synth import config
     inst = config(name)
-    ctx = _ctx(gpu_lib, inst)
+    ctx = _ctx(gpu_lib, inst, kernel)
     N = 1000 if name == "C1" else 1000
     Z, _ = ctx.debug_descent(N, 0, N, T, inst.lr, 11)
     _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, 11, np.arange(N))
@@ -57,31 +63,33 @@ def test_descent_iterates_small_T_all_starts(gpu_lib, name, T):
     assert _pass_frac(Z, Zo) >= 0.999
 
 
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,T", [("C1", 50), ("C1", 200), ("C2a", 50), ("C2a", 200)])
-def test_descent_iterates_gate_g2(gpu_lib, name, T):
+def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
     """pass_frac(GPU vs fp64) >= pass_frac(fp32 oracle vs fp64) - 0.01 (the method is chaotic: even exact
     fp32 arithmetic loses 1e-4 agreement on some starts)."""
     from synth import config
     inst = config(name)
-    ctx = _ctx(gpu_lib, inst)
+    ctx = _ctx(gpu_lib, inst, kernel)
     N = 1024
     Z, _ = ctx.debug_descent(N, 0, N, T, inst.lr, inst.seed)
     _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
     Z64 = OX.descend(z0, ctx.B, T, inst.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, T, inst.lr, dtype=np.float32)
     gpu, ref = _pass_frac(Z, Z64), _pass_frac(Z32, Z64)
-    print(f"{name} T={T}: gpu pass {gpu:.4f}, fp32-oracle pass {ref:.4f}")
+    print(f"{name} T={T} kernel={kernel}: gpu pass {gpu:.4f}, fp32-oracle pass {ref:.4f}")
     assert gpu >= ref - 0.01
 
 
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,N,filt", [("C1", 1024, 1), ("C1", 1024, 0), ("C2a", 1024, 1), ("C2a", 1024, 0),
                                          ("C2b", 512, 1)])
-def test_postprocess_bit_exact_on_gpu_candidates(gpu_lib, name, N, filt):
+def test_postprocess_bit_exact_on_gpu_candidates(gpu_lib, name, N, filt, kernel):
     """G1: the oracle's check -> dedupe -> ⊑ filter -> lex sort of the GPU's candidate multiset equals the
     GPU's output byte for byte."""
     from synth import config
     inst = config(name)
-    ctx = _ctx(gpu_lib, inst)
+    ctx = _ctx(gpu_lib, inst, kernel)
     ctx.set_params(filter_minimal=bool(filt))
     ctx.set_debug(True)
     ds = ctx.extract(N, inst.steps, inst.lr, inst.seed)
@@ -94,17 +102,18 @@ def test_postprocess_bit_exact_on_gpu_candidates(gpu_lib, name, N, filt):
     assert ds.pool_size == len(OP.dedupe(cand))
 
 
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,N", [("C1", 1024), ("C2a", 1024)])
-def test_sets_match_oracle_g3(gpu_lib, name, N):
+def test_sets_match_oracle_g3(gpu_lib, name, N, kernel):
     from synth import config
     inst = config(name)
-    ctx = _ctx(gpu_lib, inst)
+    ctx = _ctx(gpu_lib, inst, kernel)
     ds = ctx.extract(N, inst.steps, inst.lr, inst.seed)
     gpu_min = _set(ds.rows())
     pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
     ora_min = OP.minimal_filter(pool)
     j = _jaccard(gpu_min, ora_min)
-    print(f"{name}: |gpu|={len(gpu_min)} |oracle|={len(ora_min)} jaccard={j:.4f}")
+    print(f"{name} kernel={kernel}: |gpu|={len(gpu_min)} |oracle|={len(ora_min)} jaccard={j:.4f}")
     assert j >= 0.99
     diff = np.array(sorted(gpu_min ^ ora_min), dtype=np.int64).reshape(-1, inst.n)
     if diff.size:
@@ -203,3 +212,29 @@ def test_extract_errors(gpu_lib):
     with pytest.raises(gpu_lib.MapleError) as e:
         ctx.set_params(lambda1=-1.0)
     assert e.value.name == "BAD_ARG"
+
+
+def test_umma_selftest_exact(gpu_lib):
+    """tcgen05 descriptors and operand layout: single-tile products of small integers are exact."""
+    rng = np.random.default_rng(0)
+    A1 = rng.integers(-3, 4, size=(128, 48)).astype(np.float32)
+    B1 = rng.integers(-3, 4, size=(64, 48)).astype(np.float32)
+    A2 = rng.integers(-3, 4, size=(128, 64)).astype(np.float32)
+    B2 = rng.integers(-3, 4, size=(48, 64)).astype(np.float32)
+    D1, D2 = gpu_lib.maple_selftest_umma(A1, B1, A2, B2)
+    np.testing.assert_array_equal(D1, A1 @ B1.T)
+    np.testing.assert_array_equal(D2, A2 @ B2.T)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2a"])
+def test_tc_and_simt_kernels_agree(gpu_lib, name):
+    """Both descent kernels implement the same fp32 algorithm: iterates agree at small T for every start,
+    and the extracted ⊑-minimal sets agree at the stated T."""
+    from synth import config
+    inst = config(name)
+    a, b = _ctx(gpu_lib, inst, SIMT), _ctx(gpu_lib, inst, TC)
+    Za, _ = a.debug_descent(777, 0, 777, 10, inst.lr, 3)
+    Zb, _ = b.debug_descent(777, 0, 777, 10, inst.lr, 3)
+    assert _pass_frac(Zb, Za.astype(np.float64)) >= 0.999
+    sa, sb = _set(a.extract(2048, inst.steps, inst.lr, 3).rows()), _set(b.extract(2048, inst.steps, inst.lr, 3).rows())
+    assert _jaccard(sa, sb) >= 0.99
