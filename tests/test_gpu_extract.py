@@ -153,7 +153,7 @@ def test_merge_edge_cases_bit_exact(gpu_lib, k, filt):
     box = inst.u - inst.l
     rows = _random_kernel_rows(ctx.B, box, max(k, 1), seed=k)[:k] if k else np.zeros((0, inst.n), np.int64)
     if k >= 2:  # a few invalid rows: not in the kernel, out of the box, zero
-        bad = rows[:3].copy()
+        bad = np.repeat(rows[:1], 3, axis=0)
         bad[0, 0] += 1
         bad[1, :] = 0
         bad[2, 0] = box[0] + 1 if box[0] < 127 else bad[2, 0]
