@@ -58,7 +58,7 @@ struct maple_ctx {
     std::vector<int64_t> B;       // n x d
     std::vector<double> Bp;       // d x n
     // device constants
-    DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, bit_coord, bit_k;
+    DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, th_off, th_c0, th_c1;
     int nnz = 0, Lh = 0, Wh = 0;
     double rbound = 0;            // max_j sum_i |B+_ji| (u_i - l_i): bound on |round(z)| of any in-box g
     // params (Eq. 3 / Adam)
@@ -87,6 +87,10 @@ struct maple_dirset {
     int64_t size = 0, pool_size = 0, n_bad = 0;
     int8_t* rows = nullptr;       // size x n_pad, canonical, lex sorted
     int8_t* D = nullptr;          // 2*size x n_pad: rows ∪ -rows, lex sorted (lazily built)
+    int32_t* D_nnz = nullptr;     // ELL of D (lazily built)
+    int16_t* D_col = nullptr;
+    int8_t* D_val = nullptr;
+    int D_nzmax = 0;
 };
 
 // counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
@@ -197,7 +201,8 @@ int finish_set(maple_ctx* ctx, int64_t pool_count, int filter_minimal, maple_dir
     if (K > 0) ctx->launches++;
     CU(cudaEventRecord(ctx->ev[3], s));
     if (filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
-    FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->bit_coord.as<int32_t>(), ctx->bit_k.as<int32_t>(),
+    FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
+                  ctx->th_c1.as<int32_t>(),
                   ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
                   ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh};
@@ -288,14 +293,15 @@ int insert_rows_and_finish(maple_ctx* ctx, const int8_t* drows, int64_t k, int s
 }
 
 int build_step_table(maple_ctx* ctx, int T, double lr) {
-    std::vector<float2> tab(T);
+    // per step t: (lr / (1 - beta1^t), sqrt(1 - beta2^t), 1 / sqrt(1 - beta2^t)) computed in fp64 (torch scalars)
+    std::vector<float4> tab(T);
     for (int t = 1; t <= T; ++t) {
         const double bc1 = 1.0 - std::pow(ctx->beta1, t);
-        const double bc2 = 1.0 - std::pow(ctx->beta2, t);
-        tab[t - 1] = make_float2((float)(lr / bc1), (float)std::sqrt(bc2));
+        const double bc2s = std::sqrt(1.0 - std::pow(ctx->beta2, t));
+        tab[t - 1] = make_float4((float)(lr / bc1), (float)bc2s, (float)(1.0 / bc2s), 0.f);
     }
-    CU(ctx->step_tab.ensure(sizeof(float2) * T));
-    CU(cudaMemcpyAsync(ctx->step_tab.p, tab.data(), sizeof(float2) * T, cudaMemcpyHostToDevice, ctx->stream));
+    CU(ctx->step_tab.ensure(sizeof(float4) * T));
+    CU(cudaMemcpyAsync(ctx->step_tab.p, tab.data(), sizeof(float4) * T, cudaMemcpyHostToDevice, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return MAPLE_OK;
 }
@@ -313,7 +319,7 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.eps = (float)ctx->eps;
     p.omb1 = (float)(1.0 - ctx->beta1);
     p.omb2 = (float)(1.0 - ctx->beta2);
-    p.step_tab = ctx->step_tab.as<float2>();
+    p.step_tab = ctx->step_tab.as<float4>();
     p.seed = seed;
     p.n_total = n_total;
     p.begin = begin;
@@ -417,15 +423,28 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
             bdn[(size_t)j * n + i] = (float)v;
             b8[(size_t)i * d + j] = (int8_t)v;
         }
-    // thermometer bit map (filter): P half has Lh = sum(u - l) bits
-    std::vector<int32_t> bc, bk;
-    for (int i = 0; i < n; ++i)
-        for (int k = 1; k <= ctx->box[i]; ++k) {
-            bc.push_back(i);
-            bk.push_back(k);
-        }
-    ctx->Lh = (int)bc.size();
+    // thermometer code map (filter): coordinate i owns bits [off_i, off_i + u_i - l_i) of each half
+    std::vector<int32_t> toff(n);
+    int lh = 0;
+    for (int i = 0; i < n; ++i) {
+        toff[i] = lh;
+        lh += ctx->box[i];
+    }
+    ctx->Lh = lh;
     ctx->Wh = (ctx->Lh + 31) / 32;
+    std::vector<int32_t> wc0(std::max(ctx->Wh, 1), 0), wc1(std::max(ctx->Wh, 1), -1);
+    for (int w = 0; w < ctx->Wh; ++w) {
+        int c0 = -1, c1 = -1;
+        for (int i = 0; i < n; ++i) {
+            const int b0 = toff[i], b1 = toff[i] + ctx->box[i];
+            if (b1 > 32 * w && b0 < 32 * (w + 1) && b1 > b0) {
+                if (c0 < 0) c0 = i;
+                c1 = i;
+            }
+        }
+        wc0[w] = c0 < 0 ? 0 : c0;
+        wc1[w] = c1;
+    }
     CU(upload(ctx->A_rowptr, rp));
     CU(upload(ctx->A_col, col));
     CU(upload(ctx->A_val, val));
@@ -436,8 +455,9 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->B_dn, bdn));
     CU(upload(ctx->B8, b8));
     CU(upload(ctx->dBp, ctx->Bp));
-    CU(upload(ctx->bit_coord, bc));
-    CU(upload(ctx->bit_k, bk));
+    CU(upload(ctx->th_off, toff));
+    CU(upload(ctx->th_c0, wc0));
+    CU(upload(ctx->th_c1, wc1));
     CU(ctx->counters.ensure(sizeof(unsigned long long) * C_N));
     CU(cudaMemset(ctx->counters.p, 0, sizeof(unsigned long long) * C_N));
     *out = hold.release();
@@ -468,7 +488,7 @@ void maple_destroy(maple_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
-                      &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->bit_coord, &ctx->bit_k, &ctx->step_tab, &ctx->cand,
+                      &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
@@ -711,6 +731,9 @@ void maple_dirset_free(maple_dirset* ds) {
     if (!ds) return;
     if (ds->rows) cudaFree(ds->rows);
     if (ds->D) cudaFree(ds->D);
+    if (ds->D_nnz) cudaFree(ds->D_nnz);
+    if (ds->D_col) cudaFree(ds->D_col);
+    if (ds->D_val) cudaFree(ds->D_val);
     delete ds;
 }
 
@@ -788,14 +811,26 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
         ctx->launches += nl;
         CU(cudaStreamSynchronize(s));
         un.release();
+        CU(cudaMalloc(&dsm->D_nnz, (size_t)2 * K * sizeof(int32_t)));
+        DevBuf nzd;
+        CU(nzd.ensure(sizeof(int)));
+        CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, dsm->D_nnz, nzd.as<int>(), &dsm->D_col, &dsm->D_val,
+                              &dsm->D_nzmax, s));
+        ctx->launches += 2;
+        CU(cudaStreamSynchronize(s));
+        nzd.release();
     }
     // objective data (dense Q per instance)
     std::vector<double> Q((size_t)n_inst * n * n, 0.0), c((size_t)n_inst * n), c0(n_inst);
     for (int t = 0; t < n_inst; ++t) {
         double* Qt = Q.data() + (size_t)t * n * n;
-        if (f[t].kind == MAPLE_OBJ_QUADRATIC)
-            std::memcpy(Qt, f[t].Q, sizeof(double) * n * n);
-        else
+        if (f[t].kind == MAPLE_OBJ_QUADRATIC) {
+            // the kernels use grad = Q x + c, which is the gradient of 1/2 x^T Q x only for symmetric Q:
+            // use the symmetric part (same objective values, exact in fp64 for integer data)
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    Qt[(size_t)i * n + j] = 0.5 * (f[t].Q[(size_t)i * n + j] + f[t].Q[(size_t)j * n + i]);
+        } else
             for (int i = 0; i < n; ++i) Qt[(size_t)i * n + i] = f[t].Q[i];
         std::memcpy(c.data() + (size_t)t * n, f[t].c, sizeof(double) * n);
         c0[t] = f[t].c0;
@@ -820,6 +855,10 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     p.n_pad = np;
     p.n_dir = (int)K;
     p.dirs = dsm->D;
+    p.nnz = dsm->D_nnz;
+    p.col = dsm->D_col;
+    p.val = dsm->D_val;
+    p.nzmax = dsm->D_nzmax;
     p.Q = ctx->aQ.as<double>();
     p.c = ctx->ac.as<double>();
     p.c0 = ctx->ac0.as<double>();

@@ -7,6 +7,9 @@
 // 1..λmax(x, g) that keep l <= x + λg <= u (A g = 0 keeps A x = b). The CTA takes the argmin over
 // (2Δ, index of g in D, λ) among strict improvements 2Δ < 0 — the paper's argmin with the tie-break of
 // reading #17 — applies x += λg and ∇ += λ Q g, and stops when no improving step exists.
+// Directions are kept in ELL form (nonzero columns + values, Graver elements are sparse), so the score,
+// the step bound and the gradient update all cost O(nnz(g)) instead of O(n).
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 
@@ -20,25 +23,47 @@ namespace {
 constexpr int kAugThreads = 256;
 constexpr int kMaxN = 1024;
 
-// q_e = g_e^T Q g_e for every direction of D (per instance)
+// ELL of D: for each row e, nnz[e] <= nzmax columns (ascending) and values
+__global__ void ell_count_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nD; e += gridDim.x * blockDim.x) {
+        const int8_t* g = dirs + (size_t)e * n_pad;
+        int c = 0;
+        for (int i = 0; i < n; ++i) c += g[i] != 0;
+        nnz[e] = c;
+        atomicMax(nzmax, c);
+    }
+}
+
+__global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int nzmax, int16_t* col,
+                                int8_t* val) {
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nD; e += gridDim.x * blockDim.x) {
+        const int8_t* g = dirs + (size_t)e * n_pad;
+        int c = 0;
+        for (int i = 0; i < n; ++i)
+            if (g[i]) {
+                col[(size_t)e * nzmax + c] = (int16_t)i;
+                val[(size_t)e * nzmax + c] = g[i];
+                ++c;
+            }
+    }
+}
+
+// q_e = g_e^T Q g_e for every direction of D (per instance), over the nonzeros of g_e
 __global__ void qg_kernel(AugmentParams p) {
     const int nD = 2 * p.n_dir;
     const int64_t total = (int64_t)nD * p.n_inst;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int inst = (int)(t / nD);
         const int e = (int)(t % nD);
-        const int8_t* g = p.dirs + (size_t)e * p.n_pad;
         const double* Q = p.Q + (size_t)inst * p.n * p.n;
+        const int k = p.nnz[e];
+        const int16_t* cl = p.col + (size_t)e * p.nzmax;
+        const int8_t* vl = p.val + (size_t)e * p.nzmax;
         double acc = 0.0;
-        for (int i = 0; i < p.n; ++i) {
-            const int gi = g[i];
-            if (!gi) continue;
+        for (int a = 0; a < k; ++a) {
             double row = 0.0;
-            for (int j = 0; j < p.n; ++j) {
-                const int gj = g[j];
-                if (gj) row += Q[(size_t)i * p.n + j] * (double)gj;
-            }
-            acc += (double)gi * row;
+            for (int b = 0; b < k; ++b) row += Q[(size_t)cl[a] * p.n + cl[b]] * (double)vl[b];
+            acc += (double)vl[a] * row;
         }
         const_cast<double*>(p.qg)[(size_t)inst * nD + e] = acc;
     }
@@ -91,12 +116,13 @@ augment_kernel(AugmentParams p) {
     for (; it < p.max_iter; ++it) {
         Cand mine{DBL_MAX, 0x7fffffff, 0x7fffffff};
         for (int e = threadIdx.x; e < nD; e += blockDim.x) {
-            const int8_t* g = p.dirs + (size_t)e * p.n_pad;
+            const int k = p.nnz[e];
+            const int16_t* cl = p.col + (size_t)e * p.nzmax;
+            const int8_t* vl = p.val + (size_t)e * p.nzmax;
             double s = 0.0;
             int lmax = 0x7fffffff;
-            for (int i = 0; i < n; ++i) {
-                const int gi = g[i];
-                if (!gi) continue;
+            for (int a = 0; a < k; ++a) {
+                const int i = cl[a], gi = vl[a];
                 s += (double)gi * grad[i];
                 const int room = gi > 0 ? (p.hi[i] - x[i]) / gi : (x[i] - p.lo[i]) / (-gi);
                 lmax = min(lmax, room);
@@ -131,18 +157,17 @@ augment_kernel(AugmentParams p) {
         __syncthreads();
         const Cand b = best_sh;
         if (b.e == 0x7fffffff) break;  // no improving step: x is Graver-optimal w.r.t. D
-        const int8_t* g = p.dirs + (size_t)b.e * p.n_pad;
-        // ∇ += λ Q g
+        const int k = p.nnz[b.e];
+        const int16_t* cl = p.col + (size_t)b.e * p.nzmax;
+        const int8_t* vl = p.val + (size_t)b.e * p.nzmax;
+        // ∇ += λ Q g (Q symmetric: column cl[a] of Q = row cl[a], read coalesced)
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             double acc = 0.0;
-            for (int j = 0; j < n; ++j) {
-                const int gj = g[j];
-                if (gj) acc += Q[(size_t)i * n + j] * (double)gj;
-            }
+            for (int a = 0; a < k; ++a) acc += Q[(size_t)cl[a] * n + i] * (double)vl[a];
             grad[i] += (double)b.lam * acc;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] += b.lam * (int)g[i];
+        for (int a = threadIdx.x; a < k; a += blockDim.x) x[cl[a]] += b.lam * (int)vl[a];
         if (threadIdx.x == 0) f2_sh += b.key;
         __syncthreads();
     }
@@ -153,35 +178,62 @@ augment_kernel(AugmentParams p) {
     }
 }
 
-// per instance: the best final incumbent (min 2f, ties lexicographically smallest x; reading #19)
+__device__ __forceinline__ bool inc_better(const AugmentParams& p, int a, int b) {
+    if (b < 0) return a >= 0;
+    if (a < 0) return false;
+    const double fa = p.F2[a], fb = p.F2[b];
+    if (fa != fb) return fa < fb;
+    const int32_t* xa = p.X + (size_t)a * p.n;
+    const int32_t* xb = p.X + (size_t)b * p.n;
+    for (int i = 0; i < p.n; ++i)
+        if (xa[i] != xb[i]) return xa[i] < xb[i];
+    return a < b;
+}
+
+// per instance (one block): the best final incumbent (min 2f, ties lexicographically smallest x; reading #19)
 __global__ void best_kernel(AugmentParams p, int32_t* xbest, double* f2best) {
-    for (int inst = blockIdx.x * blockDim.x + threadIdx.x; inst < p.n_inst; inst += gridDim.x * blockDim.x) {
-        int b = 0;
-        const int base = inst * p.k0;
-        for (int k = 1; k < p.k0; ++k) {
-            const double fk = p.F2[base + k], fb = p.F2[base + b];
-            bool take = fk < fb;
-            if (fk == fb) {
-                const int32_t* xa = p.X + (size_t)(base + k) * p.n;
-                const int32_t* xb = p.X + (size_t)(base + b) * p.n;
-                for (int i = 0; i < p.n; ++i)
-                    if (xa[i] != xb[i]) {
-                        take = xa[i] < xb[i];
-                        break;
-                    }
-            }
-            if (take) b = k;
-        }
-        for (int i = 0; i < p.n; ++i) xbest[(size_t)inst * p.n + i] = p.X[(size_t)(base + b) * p.n + i];
-        f2best[inst] = p.F2[base + b];
+    __shared__ int cand[128];
+    const int inst = blockIdx.x;
+    const int base = inst * p.k0;
+    int b = -1;
+    for (int k = threadIdx.x; k < p.k0; k += blockDim.x)
+        if (inc_better(p, base + k, b)) b = base + k;
+    cand[threadIdx.x] = b;
+    __syncthreads();
+    for (int w = 64; w > 0; w >>= 1) {
+        if (threadIdx.x < w && inc_better(p, cand[threadIdx.x + w], cand[threadIdx.x])) cand[threadIdx.x] = cand[threadIdx.x + w];
+        __syncthreads();
     }
+    const int bb = cand[0];
+    for (int i = threadIdx.x; i < p.n; i += blockDim.x) xbest[(size_t)inst * p.n + i] = p.X[(size_t)bb * p.n + i];
+    if (threadIdx.x == 0) f2best[inst] = p.F2[bb];
 }
 
 }  // namespace
 
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax_dev,
+                               int16_t** col, int8_t** val, int* nzmax_host, cudaStream_t s) {
+    if (nD <= 0) {
+        *nzmax_host = 0;
+        return cudaSuccess;
+    }
+    cudaError_t e = cudaMemsetAsync(nzmax_dev, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+    const unsigned blocks = (unsigned)std::min(148 * 8, (nD + 255) / 256);
+    ell_count_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, nnz, nzmax_dev);
+    if ((e = cudaMemcpyAsync(nzmax_host, nzmax_dev, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+    const int nz = std::max(*nzmax_host, 1);
+    if ((e = cudaMalloc(col, (size_t)nD * nz * sizeof(int16_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(val, (size_t)nD * nz)) != cudaSuccess) return e;
+    ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, nz, *col, *val);
+    *nzmax_host = nz;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s) {
     if (p.n_inst <= 0 || p.k0 <= 0) return cudaSuccess;
-    best_kernel<<<(p.n_inst + 127) / 128, 128, 0, s>>>(p, xbest, f2best);
+    best_kernel<<<p.n_inst, 128, 0, s>>>(p, xbest, f2best);
     return cudaGetLastError();
 }
 

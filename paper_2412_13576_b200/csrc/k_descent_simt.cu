@@ -108,7 +108,7 @@ descent_simt_kernel(const DescentParams p) {
             }
         }
         // Adam (reading #9)
-        const float2 st = p.step_tab[t];
+        const float4 st = p.step_tab[t];
 #pragma unroll
         for (int q = 0; q < QD; ++q) {
             const int j = lane + 32 * q;

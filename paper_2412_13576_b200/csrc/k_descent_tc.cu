@@ -31,29 +31,38 @@ constexpr int kRows = 128;
 constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 256;
 
-__host__ __device__ constexpr uint32_t al1k(uint32_t x) { return (x + 1023u) & ~1023u; }
+__host__ __device__ constexpr uint32_t al128(uint32_t x) { return (x + 127u) & ~127u; }
 
 template <int NP, int DP>
 struct Lay {
     static constexpr int NH = NP / 2, DH = DP / 2;
     static constexpr uint32_t B32 = 0;                                   // NP x DP tf32 (forward B)
-    static constexpr uint32_t B16 = al1k(B32 + NP * DP * 4);             // NP x DP f16 (harvest B)
-    static constexpr uint32_t BT16 = al1k(B16 + NP * DP * 2);            // DP x NP f16 (backward B)
-    static constexpr uint32_t ZHI = al1k(BT16 + DP * NP * 2);            // 128 x DP tf32 (A, hi)
-    static constexpr uint32_t ZLO = al1k(ZHI + kRows * DP * 4);          // 128 x DP tf32 (A, lo)
-    static constexpr uint32_t R16 = al1k(ZLO + kRows * DP * 4);          // 128 x DP f16 (A, harvest)
-    static constexpr uint32_t S16 = al1k(R16 + kRows * DP * 2);          // 128 x NP f16 (A, backward)
-    static constexpr uint32_t GB = al1k(S16 + kRows * NP * 2);           // 128 x NP int8 harvested rows
-    static constexpr uint32_t BOX = al1k(GB + kRows * NP);               // NP int32
-    static constexpr uint32_t PAIR = al1k(BOX + NP * 4);                 // pair exchange
-    static constexpr uint32_t PAIR_BYTES = 2 * 2 * kRows * 4 * 2 + 3 * 2 * kRows;
-    static constexpr uint32_t G0_ALIAS = ZHI;                            // fp64 128 x (NP+1) staging
-    static constexpr uint32_t G0_BYTES = kRows * (NP + 1) * 8;
-    static constexpr bool G0_FITS = G0_BYTES <= GB - ZHI;
-    static constexpr uint32_t G0 = G0_FITS ? G0_ALIAS : al1k(PAIR + PAIR_BYTES);
-    static constexpr uint32_t MBAR = al1k((G0_FITS ? PAIR + PAIR_BYTES : G0 + G0_BYTES));
+    static constexpr uint32_t B16 = al128(B32 + NP * DP * 4);            // NP x DP f16 (harvest B)
+    static constexpr uint32_t BT16 = al128(B16 + NP * DP * 2);           // DP x NP f16 (backward B)
+    static constexpr uint32_t ZHI = al128(BT16 + DP * NP * 2);           // 128 x DP tf32 (A, hi)
+    static constexpr uint32_t ZLO = al128(ZHI + kRows * DP * 4);         // 128 x DP tf32 (A, lo)
+    static constexpr uint32_t R16 = al128(ZLO + kRows * DP * 4);         // 128 x DP f16 (A, harvest)
+    static constexpr uint32_t S16 = al128(R16 + kRows * DP * 2);         // 128 x NP f16 (A, backward)
+    static constexpr uint32_t BOX = al128(S16 + kRows * NP * 2);         // NP f32 (u - l)
+    static constexpr uint32_t PAIR = al128(BOX + NP * 4);                // pair exchange
+    static constexpr uint32_t PAIR_BYTES = 2 * 2 * kRows * 4 * 2 + 2 * kRows;
+    static constexpr int KC = 16;                                        // g0 staging chunk (coordinates)
+    static constexpr uint32_t G0_BYTES = kRows * (KC + 1) * 8;           // fp64 start staging
+    static constexpr bool G0_FITS = G0_BYTES <= BOX - ZHI;
+    static constexpr uint32_t G0 = G0_FITS ? ZHI : al128(PAIR + PAIR_BYTES);
+    static constexpr uint32_t MBAR = al128(G0_FITS ? PAIR + PAIR_BYTES : G0 + G0_BYTES);
     static constexpr uint32_t TOTAL = MBAR + 64;
+    // TMEM columns: G | X (harvest H, then Γ) | m | v
+    static constexpr uint32_t XW = NP > DP ? NP : DP;
+    static constexpr uint32_t CG = 0, CX = NP, CM = NP + XW, CV = NP + XW + DP;
+    static_assert(CV + DP <= kTmemCols, "TMEM budget");
 };
+
+// f16 bit pattern of sign(y): 0x3C00 (+1), 0xBC00 (-1), 0 (y == 0, sign(0) = 0)
+__device__ __forceinline__ uint32_t sign_h(float y) {
+    const uint32_t b = __float_as_uint(y);
+    return (b << 1) ? (((b >> 16) & 0x8000u) | 0x3C00u) : 0u;
+}
 
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
     __half2 h = __floats2half2_rn(a, b);
@@ -61,9 +70,9 @@ __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
 }
 
 template <int NP, int DP>
-__global__ void __launch_bounds__(kThreads, 1) descent_tc_kernel(const DescentParams p) {
+__global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentParams p) {
     using L = Lay<NP, DP>;
-    constexpr int NH = L::NH, DH = L::DH;
+    constexpr int DH = L::DH;
     extern __shared__ __align__(1024) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int quad = warp & 3, half = warp >> 2;
@@ -73,15 +82,12 @@ __global__ void __launch_bounds__(kThreads, 1) descent_tc_kernel(const DescentPa
     const int64_t gi = p.begin + local;
     const int n = p.n, d = p.d;
 
-    float* amax = reinterpret_cast<float*>(sm + L::PAIR);        // [parity][half][row]
-    int* aidx = reinterpret_cast<int*>(amax + 2 * 2 * kRows);    // [parity][half][row]
+    float* amax = reinterpret_cast<float*>(sm + L::PAIR);             // [parity][half][row]
+    int* aidx = reinterpret_cast<int*>(amax + 2 * 2 * kRows);         // [parity][half][row]
     uint8_t* chg = reinterpret_cast<uint8_t*>(aidx + 2 * 2 * kRows);  // [half][row]
-    uint8_t* okf = chg + 2 * kRows;
-    uint8_t* nzf = okf + 2 * kRows;
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + L::MBAR);
     uint32_t* tbase_sh = reinterpret_cast<uint32_t*>(mbar + 2);
-    int32_t* boxs = reinterpret_cast<int32_t*>(sm + L::BOX);
-    int8_t* gbuf = reinterpret_cast<int8_t*>(sm + L::GB);
+    float* boxs = reinterpret_cast<float*>(sm + L::BOX);
 
     // ---- setup: TMEM, barriers, B operands (exact small integers) ----
     if (warp == 0) tmem_alloc(tbase_sh, kTmemCols);
@@ -97,85 +103,101 @@ __global__ void __launch_bounds__(kThreads, 1) descent_tc_kernel(const DescentPa
         *reinterpret_cast<__half*>(sm + L::B16 + op_offset(i, k >> 3, NP) + (k & 7) * 2) = __float2half_rn(v);
         *reinterpret_cast<__half*>(sm + L::BT16 + op_offset(k, i >> 3, DP) + (i & 7) * 2) = __float2half_rn(v);
     }
-    for (int i = tid; i < NP; i += kThreads) boxs[i] = i < n ? p.box[i] : 0;
-    // ---- starts (Alg. 3 lines 4-5): g0 in fp64 from the counter RNG, z0 = B+ g0 ----
+    for (int i = tid; i < NP; i += kThreads) boxs[i] = i < n ? (float)p.box[i] : 0.f;
+    // ---- starts (Alg. 3 lines 4-5): g0 in fp64 from the counter RNG, z0 = B+ g0 (k ascending) ----
     double* g0s = reinterpret_cast<double*>(sm + L::G0);
-    for (int k = half * NH; k < (half + 1) * NH; ++k) {
-        double g = 0.0;
-        if (active && k < n) g = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
-        g0s[row * (NP + 1) + k] = g;
+    double zacc[DH];
+#pragma unroll
+    for (int q = 0; q < DH; ++q) zacc[q] = 0.0;
+    for (int k0 = 0; k0 < n; k0 += L::KC) {
+        for (int kk = half; kk < L::KC; kk += 2) {
+            const int k = k0 + kk;
+            double g = 0.0;
+            if (active && k < n) g = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
+            g0s[row * (L::KC + 1) + kk] = g;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < DH; ++q) {
+            const int j = half * DH + q;
+            if (j < d) {
+                const double* bp = p.Bp + (size_t)j * n;
+                const int kend = min(L::KC, n - k0);
+                for (int kk = 0; kk < kend; ++kk) zacc[q] = fma(bp[k0 + kk], g0s[row * (L::KC + 1) + kk], zacc[q]);
+            }
+        }
+        __syncthreads();
     }
     fence_before();
     __syncthreads();
     fence_after();
     const uint32_t tbase = *tbase_sh;
-    float z[DH], m[DH], v[DH];
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tl = tbase + lane_off;
+    {   // m = v = 0 in TMEM
+        const uint32_t zr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int q = 0; q < DH; ++q) {
-        const int j = half * DH + q;
-        double acc = 0.0;
-        if (j < d && active) {
-            const double* bp = p.Bp + (size_t)j * n;
-            for (int k = 0; k < n; ++k) acc = fma(bp[k], g0s[row * (NP + 1) + k], acc);
-            if (p.Z0_out) p.Z0_out[local * d + j] = acc;
+        for (int c = 0; c < DH / 8; ++c) {
+            st8(tl + L::CM + half * DH + 8 * c, zr);
+            st8(tl + L::CV + half * DH + 8 * c, zr);
         }
-        z[q] = (float)acc;
-        m[q] = 0.f;
-        v[q] = 0.f;
+        st_wait();
     }
     __syncthreads();  // g0 staging may alias the operand area
-    // operands of step 1 + argmax of |z0|
-    auto write_z = [&](int parity) {
+    // The iterate lives in shared memory as the forward operand: Z_hi = tf32_rna(z) and the exact residual
+    // Z_lo = z - Z_hi (the MMA consumes its TF32 part), so z = Z_hi + Z_lo exactly. Also round(z) as f16.
+    {
         float lmax = -1.f;
         int lidx = 0;
 #pragma unroll
-        for (int c = 0; c < DH / 4; ++c) {
-            float4 hi, lo;
-            float* h = &hi.x;
-            float* o = &lo.x;
+        for (int c = 0; c < DH / 8; ++c) {
+            float4 hi[2], lo[2];
+            uint32_t rnew[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float zz = z[4 * c + e];
-                h[e] = to_tf32(zz);
-                o[e] = to_tf32(zz - h[e]);
-                const float a = fabsf(zz);
-                if (a > lmax) {
-                    lmax = a;
-                    lidx = half * DH + 4 * c + e;
+            for (int e = 0; e < 8; ++e) {
+                const int q = 8 * c + e;
+                const int j = half * DH + q;
+                const float zz = (j < d && active) ? (float)zacc[q] : 0.f;
+                if (j < d && active && p.Z0_out) p.Z0_out[local * d + j] = zacc[q];
+                (&hi[e >> 2].x)[e & 3] = tf32_rna(zz);
+                (&lo[e >> 2].x)[e & 3] = zz - tf32_rna(zz);
+                const float tq = truncf(zz), dq = zz - tq;
+                const float rq = fabsf(dq) >= 0.5f ? tq + copysignf(1.f, dq) : tq;
+                const uint32_t hb = __half_as_ushort(__float2half_rn(rq));
+                rnew[e >> 1] = (e & 1) ? (rnew[e >> 1] | (hb << 16)) : hb;
+                if (fabsf(zz) > lmax) {
+                    lmax = fabsf(zz);
+                    lidx = j;
                 }
             }
-            const uint32_t off = op_offset(row, half * (DH / 4) + c, kRows);
-            *reinterpret_cast<float4*>(sm + L::ZHI + off) = hi;
-            *reinterpret_cast<float4*>(sm + L::ZLO + off) = lo;
-        }
 #pragma unroll
-        for (int c = 0; c < DH / 8; ++c) {
-            uint4 w;
-            uint32_t* wp = &w.x;
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-                wp[e] = pack_h2((float)round_half_away(z[8 * c + 2 * e]), (float)round_half_away(z[8 * c + 2 * e + 1]));
-            *reinterpret_cast<uint4*>(sm + L::R16 + op_offset(row, half * (DH / 8) + c, kRows)) = w;
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t off = op_offset(row, half * (DH / 4) + 2 * c + u, kRows);
+                *reinterpret_cast<float4*>(sm + L::ZHI + off) = hi[u];
+                *reinterpret_cast<float4*>(sm + L::ZLO + off) = lo[u];
+            }
+            *reinterpret_cast<uint4*>(sm + L::R16 + op_offset(row, half * (DH / 8) + c, kRows)) =
+                make_uint4(rnew[0], rnew[1], rnew[2], rnew[3]);
         }
-        amax[(parity * 2 + half) * kRows + row] = lmax;
-        aidx[(parity * 2 + half) * kRows + row] = lidx;
-    };
-    write_z(0);
+        amax[(0 * 2 + half) * kRows + row] = lmax;
+        aidx[(0 * 2 + half) * kRows + row] = lidx;
+    }
 
-    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tG = tbase + lane_off, tH = tbase + NP + lane_off, tGam = tbase + 2 * NP + lane_off;
     const uint32_t sZHI = smem_u32(sm + L::ZHI), sZLO = smem_u32(sm + L::ZLO), sR = smem_u32(sm + L::R16);
     const uint32_t sS = smem_u32(sm + L::S16), sB32 = smem_u32(sm + L::B32), sB16 = smem_u32(sm + L::B16);
     const uint32_t sBT = smem_u32(sm + L::BT16);
     constexpr uint32_t LBO_A = kRows * 16, LBO_N = NP * 16, LBO_D = DP * 16, SBO = 128;
     constexpr uint32_t ID_FWD = idesc(2, kRows, NP), ID_HARV = idesc(0, kRows, NP), ID_BWD = idesc(0, kRows, DP);
+    const float lam1 = p.lam1, lam2 = p.lam2, b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, eps = p.eps;
+    const int T = p.T;
+    const bool harvest = p.harvest != 0;
+    const int64_t cap = p.cand_cap;
 
     uint32_t phA = 0, phB = 0;
-    const int T = p.T;
-    const int t_end = p.harvest ? T + 1 : T;
+    const int t_end = harvest ? T + 1 : T;
     for (int t = 1; t <= t_end; ++t) {
         const bool do_fwd = t <= T;
-        const bool do_harv = p.harvest && t >= 2;
+        const bool do_harv = harvest && t >= 2;
         fence_proxy_async();
         fence_before();
         __syncthreads();  // B1: operands written, pair info visible
@@ -184,161 +206,220 @@ __global__ void __launch_bounds__(kThreads, 1) descent_tc_kernel(const DescentPa
             if (do_fwd) {
 #pragma unroll
                 for (int kk = 0; kk < DP / 8; ++kk)
-                    mma_tf32(tbase, desc(sZHI + kk * 2 * LBO_A, LBO_A, SBO), desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO),
-                             ID_FWD, kk > 0);
+                    mma_tf32(tbase + L::CG, desc(sZHI + kk * 2 * LBO_A, LBO_A, SBO),
+                             desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < DP / 8; ++kk)
-                    mma_tf32(tbase, desc(sZLO + kk * 2 * LBO_A, LBO_A, SBO), desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO),
-                             ID_FWD, 1);
+                    mma_tf32(tbase + L::CG, desc(sZLO + kk * 2 * LBO_A, LBO_A, SBO),
+                             desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, 1);
             }
             if (do_harv) {
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk)
-                    mma_f16(tbase + NP, desc(sR + kk * 2 * LBO_A, LBO_A, SBO), desc(sB16 + kk * 2 * LBO_N, LBO_N, SBO),
-                            ID_HARV, kk > 0);
+                    mma_f16(tbase + L::CX, desc(sR + kk * 2 * LBO_A, LBO_A, SBO),
+                            desc(sB16 + kk * 2 * LBO_N, LBO_N, SBO), ID_HARV, kk > 0);
             }
             commit(&mbar[0]);
         }
         mbar_wait(&mbar[0], phA);
         phA ^= 1;
         fence_after();
-        // ---- harvest of z_{t-1}: read H only for rows whose round(z) changed ----
-        bool row_chg = false;
-        if (do_harv) {
-            const uint8_t cf = chg[row] | chg[kRows + row];
-            row_chg = active && cf == 1;
-            if (__any_sync(0xffffffffu, row_chg)) {
-                uint32_t r[NH];
-#pragma unroll
-                for (int c = 0; c < NH / 8; ++c) ld8(tH + half * NH + 8 * c, &r[8 * c]);
-#pragma unroll
-                for (int c = 0; c < NH / 8; ++c) wait8(&r[8 * c]);
-                bool ok = true, nz = false;
-#pragma unroll
-                for (int c = 0; c < NH / 4; ++c) {
-                    uint32_t w = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const int i = half * NH + 4 * c + e;
-                        const int g = (int)__uint_as_float(r[4 * c + e]);
-                        ok &= abs(g) <= boxs[i];
-                        nz |= g != 0;
-                        w |= ((uint32_t)(g & 0xFF)) << (8 * e);
-                    }
-                    *reinterpret_cast<uint32_t*>(gbuf + row * NP + half * NH + 4 * c) = w;
-                }
-                okf[half * kRows + row] = ok;
-                nzf[half * kRows + row] = nz;
-            }
-        }
-        // ---- S = sign(B z) from the forward accumulator ----
-        if (do_fwd) {
-            uint32_t r[NH];
-#pragma unroll
-            for (int c = 0; c < NH / 8; ++c) ld8(tG + half * NH + 8 * c, &r[8 * c]);
-#pragma unroll
-            for (int c = 0; c < NH / 8; ++c) wait8(&r[8 * c]);
-#pragma unroll
-            for (int c = 0; c < NH / 8; ++c) {
-                uint4 w;
-                uint32_t* wp = &w.x;
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                    wp[e] = pack_h2(fsign(__uint_as_float(r[8 * c + 2 * e])), fsign(__uint_as_float(r[8 * c + 2 * e + 1])));
-                *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, half * (NH / 8) + c, kRows)) = w;
-            }
-        }
-        fence_proxy_async();
-        fence_before();
-        __syncthreads();  // B2: S written, harvest flags visible
-        if (tid == 0 && do_fwd) {
-            fence_after();
-#pragma unroll
-            for (int kk = 0; kk < NP / 16; ++kk)
-                mma_f16(tbase + 2 * NP, desc(sS + kk * 2 * LBO_A, LBO_A, SBO), desc(sBT + kk * 2 * LBO_D, LBO_D, SBO),
-                        ID_BWD, kk > 0);
-            commit(&mbar[1]);
-        }
-        // ---- harvest write-out (half 0; overlaps the backward MMA) ----
-        if (do_harv && half == 0) {
-            const bool want = row_chg && okf[row] && okf[kRows + row] && (nzf[row] | nzf[kRows + row]);
-            const unsigned mask = __ballot_sync(0xffffffffu, want);
-            if (mask) {
-                const int leader = __ffs(mask) - 1;
-                unsigned long long base = 0;
-                if (lane == leader) base = atomicAdd(p.cand_count, (unsigned long long)__popc(mask));
-                base = __shfl_sync(0xffffffffu, base, leader);
-                if (want) {
-                    const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1u));
-                    const uint32_t* src = reinterpret_cast<const uint32_t*>(gbuf + row * NP);
+        if (half == 0) {
+            // ---- harvest of z_{t-1} (half 0, all NP columns of H): rows whose round(z) changed ----
+            if (do_harv) {
+                const uint8_t cf = chg[row] | chg[kRows + row];
+                const bool row_chg = active && cf == 1;
+                if (__any_sync(0xffffffffu, row_chg)) {
+                    uint32_t packed[NP / 4];
+                    bool ok = true, nz = false;
                     int sgn = 0;
 #pragma unroll
-                    for (int c = 0; c < NP / 4; ++c) {
-                        const uint32_t w = src[c];
-                        if (!sgn && w) sgn = ((int8_t)(w >> (8 * ((__ffs(w) - 1) >> 3)))) > 0 ? 1 : -1;
-                    }
-                    if ((int64_t)slot < p.cand_cap) {
-                        uint4* dst = reinterpret_cast<uint4*>(p.cand + (size_t)slot * p.n_pad);
-                        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+                    for (int c0 = 0; c0 < NP; c0 += 16) {
+                        constexpr int W = 16;
+                        uint32_t r[W];
 #pragma unroll
-                        for (int c = 0; c < NP / 16; ++c) {
-                            uint4 w = s4[c];
-                            if (sgn < 0) {
-                                w.x = __vneg4(w.x);
-                                w.y = __vneg4(w.y);
-                                w.z = __vneg4(w.z);
-                                w.w = __vneg4(w.w);
+                        for (int c = 0; c < W / 8; ++c) ld8(tl + L::CX + c0 + 8 * c, &r[8 * c]);
+#pragma unroll
+                        for (int c = 0; c < W / 8; ++c) wait8(&r[8 * c]);
+#pragma unroll
+                        for (int c = 0; c < W / 4; ++c) {
+                            uint32_t w = 0;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float g = __uint_as_float(r[4 * c + e]);
+                                ok &= fabsf(g) <= boxs[c0 + 4 * c + e];
+                                nz |= g != 0.f;
+                                if (!sgn && g != 0.f) sgn = g > 0.f ? 1 : -1;
+                                // exact small integer -> low byte via the 1.5 * 2^23 magic constant
+                                w |= (__float_as_uint(g + 12582912.f) & 0xFFu) << (8 * e);
                             }
-                            dst[c] = w;
+                            packed[c0 / 4 + c] = w;
+                        }
+                    }
+                    const bool want = row_chg && ok && nz;
+                    const unsigned mask = __ballot_sync(0xffffffffu, want);
+                    if (mask) {
+                        const int leader = __ffs(mask) - 1;
+                        unsigned long long base = 0;
+                        if (lane == leader) base = atomicAdd(p.cand_count, (unsigned long long)__popc(mask));
+                        base = __shfl_sync(0xffffffffu, base, leader);
+                        if (want) {
+                            const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1u));
+                            if ((int64_t)slot < cap) {
+                                uint4* dst = reinterpret_cast<uint4*>(p.cand + (size_t)slot * p.n_pad);
+#pragma unroll
+                                for (int c = 0; c < NP / 16; ++c) {
+                                    uint4 w = make_uint4(packed[4 * c], packed[4 * c + 1], packed[4 * c + 2],
+                                                         packed[4 * c + 3]);
+                                    if (sgn < 0) {
+                                        w.x = __vneg4(w.x);
+                                        w.y = __vneg4(w.y);
+                                        w.z = __vneg4(w.z);
+                                        w.w = __vneg4(w.w);
+                                    }
+                                    dst[c] = w;
+                                }
+                            }
                         }
                     }
                 }
             }
+        } else if (do_fwd) {
+            // ---- S = sign(B z) (half 1, all NP columns of G) -> f16 backward operand ----
+#pragma unroll
+            for (int c0 = 0; c0 < NP; c0 += 16) {
+                constexpr int W = 16;
+                uint32_t r[W];
+#pragma unroll
+                for (int c = 0; c < W / 8; ++c) ld8(tl + L::CG + c0 + 8 * c, &r[8 * c]);
+#pragma unroll
+                for (int c = 0; c < W / 8; ++c) wait8(&r[8 * c]);
+#pragma unroll
+                for (int c = 0; c < W / 8; ++c) {
+                    uint4 w;
+                    w.x = sign_h(__uint_as_float(r[8 * c + 0])) | (sign_h(__uint_as_float(r[8 * c + 1])) << 16);
+                    w.y = sign_h(__uint_as_float(r[8 * c + 2])) | (sign_h(__uint_as_float(r[8 * c + 3])) << 16);
+                    w.z = sign_h(__uint_as_float(r[8 * c + 4])) | (sign_h(__uint_as_float(r[8 * c + 5])) << 16);
+                    w.w = sign_h(__uint_as_float(r[8 * c + 6])) | (sign_h(__uint_as_float(r[8 * c + 7])) << 16);
+                    *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, c0 / 8 + c, kRows)) = w;
+                }
+            }
         }
         if (!do_fwd) break;
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();  // B2: S written; H consumed (its TMEM columns are reused by Γ)
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (int kk = 0; kk < NP / 16; ++kk)
+                mma_f16(tbase + L::CX, desc(sS + kk * 2 * LBO_A, LBO_A, SBO), desc(sBT + kk * 2 * LBO_D, LBO_D, SBO),
+                        ID_BWD, kk > 0);
+            commit(&mbar[1]);
+        }
         mbar_wait(&mbar[1], phB);
         phB ^= 1;
         fence_after();
-        // ---- Adam step on Γ (Eq. 3 subgradient) ----
-        uint32_t r[DH];
-#pragma unroll
-        for (int c = 0; c < DH / 8; ++c) ld8(tGam + half * DH + 8 * c, &r[8 * c]);
-#pragma unroll
-        for (int c = 0; c < DH / 8; ++c) wait8(&r[8 * c]);
+        // ---- gradient of Eq. 3 + Adam, this thread's coordinate half, 8 coordinates at a time ----
         const int par = (t - 1) & 1;
         const float a0 = amax[(par * 2 + 0) * kRows + row], a1 = amax[(par * 2 + 1) * kRows + row];
         const int i0 = aidx[(par * 2 + 0) * kRows + row], i1 = aidx[(par * 2 + 1) * kRows + row];
         const float zinf = a1 > a0 ? a1 : a0;
         const int kbest = a1 > a0 ? i1 : i0;
-        const float2 st = p.step_tab[t - 1];
-        const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2;
-        bool ch = (t == 1), big = false;
-#pragma unroll
-        for (int q = 0; q < DH; ++q) {
-            const int j = half * DH + q;
-            const float zz = z[q];
-            float g = __uint_as_float(r[q]) + p.lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
-            if (zinf < 1.f && j == kbest) g += -p.lam2 * fsign(zz) / fmaxf(zz * zz, 1e-8f);
-            m[q] = b1 * m[q] + omb1 * g;
-            v[q] = b2 * v[q] + omb2 * g * g;
-            const float denom = sqrtf(v[q]) / st.y + p.eps;
-            const float zn = zz - st.x * m[q] / denom;
-            const int rn = round_half_away(zn);
-            ch |= rn != round_half_away(zz);
-            big |= abs(rn) > 2048;
-            z[q] = zn;
+        const float4 st = p.step_tab[t - 1];     // (lr / (1 - b1^t), -, 1 / sqrt(1 - b2^t))
+        // λ2 term of Eq. 3: only on the lowest-index argmax coordinate, only while ||z||_inf < 1
+        const int kq = kbest - half * DH;  // local index (outside [0, DH) when the other half owns it)
+        float extra = 0.f;
+        if (zinf < 1.f && kq >= 0 && kq < DH) {
+            const uint32_t off = op_offset(row, half * (DH / 4) + (kq >> 2), kRows) + (kq & 3) * 4;
+            const float zk = *reinterpret_cast<const float*>(sm + L::ZHI + off) +
+                             *reinterpret_cast<const float*>(sm + L::ZLO + off);
+            if (zk != 0.f) extra = -lam2 * copysignf(1.f, zk) / fmaxf(zk * zk, 1e-8f);
         }
+        bool ch = (t == 1), big = false;
+        float lmax = -1.f;
+        int lidx = 0;
+#pragma unroll
+        for (int c = 0; c < DH / 8; ++c) {
+            uint32_t rg[8], rm[8], rv[8];
+            ld8(tl + L::CX + half * DH + 8 * c, rg);
+            ld8(tl + L::CM + half * DH + 8 * c, rm);
+            ld8(tl + L::CV + half * DH + 8 * c, rv);
+            // current iterate z = Z_hi + Z_lo and r = round(z) (the f16 harvest operand written last step)
+            const uint32_t roff = op_offset(row, half * (DH / 8) + c, kRows);
+            const uint4 rw = *reinterpret_cast<const uint4*>(sm + L::R16 + roff);
+            const uint32_t* rwp = &rw.x;
+            float4 hi[2], lo[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t off = op_offset(row, half * (DH / 4) + 2 * c + u, kRows);
+                hi[u] = *reinterpret_cast<const float4*>(sm + L::ZHI + off);
+                lo[u] = *reinterpret_cast<const float4*>(sm + L::ZLO + off);
+            }
+            wait8(rg);
+            wait8(rm);
+            wait8(rv);
+            uint32_t rnew[4];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int q = 8 * c + e;
+                float* hp = &hi[e >> 2].x;
+                float* lp = &lo[e >> 2].x;
+                const float zz = hp[e & 3] + lp[e & 3];                      // exact
+                const __half2 h2 = *reinterpret_cast<const __half2*>(&rwp[e >> 1]);
+                const float ro = (e & 1) ? __high2float(h2) : __low2float(h2);
+                const float dd = zz - ro;                                   // in [-1/2, 1/2], exact
+                const float sd = dd > 0.f ? 1.f : (dd < 0.f ? -1.f : 0.f);
+                // λ1 d/dz (z - floor z)(ceil z - z) = ceil z + floor z - 2z = sign(z - r) - 2 (z - r), r = round(z)
+                float g = fmaf(lam1, fmaf(-2.f, dd, sd), __uint_as_float(rg[e]));
+                if (q == kq) g += extra;
+                const float mm = fmaf(b1, __uint_as_float(rm[e]), omb1 * g);
+                const float vv = fmaf(b2, __uint_as_float(rv[e]), omb2 * g * g);
+                rm[e] = __float_as_uint(mm);
+                rv[e] = __float_as_uint(vv);
+                const float den = fmaf(sqrt_approx(vv), st.z, eps);
+                const float zn = fmaf(-st.x * mm, rcp_approx(den), zz);
+                const float tn = truncf(zn);
+                const float dn = zn - tn;
+                const float rn = fabsf(dn) >= 0.5f ? tn + copysignf(1.f, dn) : tn;   // round half away
+                ch |= rn != ro;
+                big |= fabsf(rn) > 2048.f;
+                const float a = fabsf(zn);
+                if (a > lmax) {
+                    lmax = a;
+                    lidx = half * DH + q;
+                }
+                hp[e & 3] = tf32_rna(zn);
+                lp[e & 3] = zn - hp[e & 3];
+                const uint32_t hb = __half_as_ushort(__float2half_rn(rn));
+                rnew[e >> 1] = (e & 1) ? (rnew[e >> 1] | (hb << 16)) : hb;
+            }
+            st8(tl + L::CM + half * DH + 8 * c, rm);
+            st8(tl + L::CV + half * DH + 8 * c, rv);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t off = op_offset(row, half * (DH / 4) + 2 * c + u, kRows);
+                *reinterpret_cast<float4*>(sm + L::ZHI + off) = hi[u];
+                *reinterpret_cast<float4*>(sm + L::ZLO + off) = lo[u];
+            }
+            *reinterpret_cast<uint4*>(sm + L::R16 + roff) = make_uint4(rnew[0], rnew[1], rnew[2], rnew[3]);
+        }
+        st_wait();
+        amax[((t & 1) * 2 + half) * kRows + row] = lmax;
+        aidx[((t & 1) * 2 + half) * kRows + row] = lidx;
         // bit 0: round(z) changed; bit 1: some |round(z_j)| > 2048 (not exact in the f16 harvest operand).
-        // The host only selects this kernel when max_j sum_i |B+_ji| (u_i - l_i) < 2048, so such an
-        // iterate cannot map to a g inside the box and skipping it is exact.
+        // The host selects this kernel only when max_j sum_i |B+_ji| (u_i - l_i) < 2048, so such an iterate
+        // cannot map to a g inside the box and skipping it is exact.
         chg[half * kRows + row] = (uint8_t)((ch ? 1 : 0) | (big ? 2 : 0));
-        write_z(t & 1);
     }
     if (p.Z_out && active) {
 #pragma unroll
         for (int q = 0; q < DH; ++q) {
             const int j = half * DH + q;
-            if (j < d) p.Z_out[local * d + j] = z[q];
+            const uint32_t off = op_offset(row, half * (DH / 4) + (q >> 2), kRows) + (q & 3) * 4;
+            if (j < d)
+                p.Z_out[local * d + j] = *reinterpret_cast<const float*>(sm + L::ZHI + off) +
+                                         *reinterpret_cast<const float*>(sm + L::ZLO + off);
         }
     }
     fence_before();

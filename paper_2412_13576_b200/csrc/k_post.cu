@@ -11,6 +11,7 @@
 //           Only rows with strictly smaller L1 norm can dominate, so rows are bucketed by L1 (counting
 //           sort) and each g scans the lower buckets tile by tile with block-wide early exit.
 //  sort     bottom-up merge sort of row indices on big-endian biased keys (lexicographic int8 order).
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -78,47 +79,55 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, int64_t count, in
     }
 }
 
-__global__ void check_kernel(const int8_t* __restrict__ rows, int64_t count, CheckParams cp, uint8_t* flags,
-                             unsigned long long* n_bad, int smem_ok) {
-    extern __shared__ int32_t sh[];
-    const int32_t* rp = cp.A_rowptr;
-    const int32_t* col = cp.A_col;
-    const int32_t* val = cp.A_val;
-    if (smem_ok) {
-        int32_t* srp = sh;
-        int32_t* scol = sh + cp.m + 1;
-        int32_t* sval = scol + cp.nnz;
-        for (int i = threadIdx.x; i <= cp.m; i += blockDim.x) srp[i] = cp.A_rowptr[i];
-        for (int i = threadIdx.x; i < cp.nnz; i += blockDim.x) {
-            scol[i] = cp.A_col[i];
-            sval[i] = cp.A_val[i];
-        }
+// (C1)-(C3): one thread per row; the block stages its rows in shared memory with coalesced 16-byte loads
+// (rows x n_pad bytes), A (CSR) sits in shared memory. Exact int64 accumulation of A g.
+constexpr int kCheckThreads = 128;
+__global__ void __launch_bounds__(kCheckThreads) check_kernel(const int8_t* __restrict__ rows, int64_t count,
+                                                              CheckParams cp, uint8_t* flags, unsigned long long* n_bad) {
+    extern __shared__ __align__(16) int32_t sh[];
+    int32_t* srp = sh;
+    int32_t* scol = srp + cp.m + 1;
+    int32_t* sval = scol + cp.nnz;
+    int32_t* sbox = sval + cp.nnz;
+    int8_t* srow = reinterpret_cast<int8_t*>(sh + (((cp.m + 1 + 2 * cp.nnz + cp.n) + 3) & ~3));
+    for (int i = threadIdx.x; i <= cp.m; i += blockDim.x) srp[i] = cp.A_rowptr[i];
+    for (int i = threadIdx.x; i < cp.nnz; i += blockDim.x) {
+        scol[i] = cp.A_col[i];
+        sval[i] = cp.A_val[i];
+    }
+    for (int i = threadIdx.x; i < cp.n; i += blockDim.x) sbox[i] = cp.box[i];
+    const int nw = cp.n_pad / 16;
+    unsigned long long bad = 0;
+    for (int64_t r0 = (int64_t)blockIdx.x * kCheckThreads; r0 < count; r0 += (int64_t)gridDim.x * kCheckThreads) {
         __syncthreads();
-        rp = srp;
-        col = scol;
-        val = sval;
-    }
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count;
-         r += (int64_t)gridDim.x * blockDim.x) {
-        const int8_t* g = rows + (size_t)r * cp.n_pad;
-        bool ok = true, nz = false;
-        for (int i = 0; i < cp.n; ++i) {
-            const int v = g[i];
-            nz |= (v != 0);
-            ok &= (abs(v) <= cp.box[i]);
+        const int64_t nr = min((int64_t)kCheckThreads, count - r0);
+        const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r0 * cp.n_pad);
+        for (int e = threadIdx.x; e < nr * nw; e += kCheckThreads) reinterpret_cast<int4*>(srow)[e] = src[e];
+        __syncthreads();
+        if (threadIdx.x < nr) {
+            const int8_t* g = srow + threadIdx.x * cp.n_pad;
+            bool ok = true, nz = false;
+            for (int i = 0; i < cp.n; ++i) {
+                const int v = g[i];
+                nz |= (v != 0);
+                ok &= (abs(v) <= sbox[i]);
+            }
+            for (int a = 0; a < cp.m && ok; ++a) {
+                long long acc = 0;
+                for (int e = srp[a]; e < srp[a + 1]; ++e) acc += (long long)sval[e] * (long long)g[scol[e]];
+                ok &= (acc == 0);
+            }
+            ok &= nz;
+            flags[r0 + threadIdx.x] = ok ? 1 : 0;
+            bad += ok ? 0 : 1;
         }
-        for (int a = 0; a < cp.m && ok; ++a) {
-            long long s = 0;
-            for (int e = rp[a]; e < rp[a + 1]; ++e) s += (long long)val[e] * (long long)g[col[e]];
-            ok &= (s == 0);
-        }
-        ok &= nz;
-        flags[r] = ok ? 1 : 0;
-        if (!ok) atomicAdd(n_bad, 1ULL);
     }
+    if (bad) atomicAdd(n_bad, bad);
 }
 
 // ---- filter ----
+// thermometer codes: thread per (row, word); word w of a half covers bits [32w, 32w+32), i.e. the coordinate
+// range [word_c0[w], word_c1[w]] (host precomputed), with bit offset off[i] = sum_{k<i} (u_k - l_k).
 __global__ void codes_kernel(const int8_t* __restrict__ rows, const uint8_t* valid, int64_t count, FilterWork fw) {
     const int W2 = 2 * fw.Wh;
     const int64_t total = count * W2;
@@ -129,26 +138,38 @@ __global__ void codes_kernel(const int8_t* __restrict__ rows, const uint8_t* val
         const int wb = neg ? w - fw.Wh : w;
         const int8_t* g = rows + (size_t)r * fw.n_pad;
         uint32_t word = 0;
-        for (int b = 0; b < 32; ++b) {
-            const int bit = wb * 32 + b;
-            if (bit >= fw.Lh) break;
-            const int v = g[fw.bit_coord[bit]];
-            const int k = fw.bit_k[bit];
-            const bool on = neg ? (v <= -k) : (v >= k);
-            word |= (on ? 1u : 0u) << b;
+        const int lo = wb * 32;
+        for (int i = fw.word_c0[wb]; i <= fw.word_c1[wb]; ++i) {
+            const int v = neg ? -(int)g[i] : (int)g[i];       // bits [off_i, off_i + v) are set
+            if (v <= 0) continue;
+            const int b0 = fw.off[i] - lo, b1 = b0 + v;          // relative to this word
+            const int a = max(b0, 0), e = min(b1, 32);
+            if (a < e) word |= (e - a == 32 ? 0xFFFFFFFFu : (((1u << (e - a)) - 1u) << a));
         }
         fw.codes[r * W2 + w] = word;
         if (w == 0) {
             int s = 0;
-            for (int i = 0; i < fw.n; ++i) s += abs((int)g[i]);
+            const int4* g4 = reinterpret_cast<const int4*>(g);
+            for (int c = 0; c < fw.n_pad / 16; ++c) {
+                const int4 q = g4[c];
+                s += (int)(__vsadu4(__vabsss4(q.x), 0) + __vsadu4(__vabsss4(q.y), 0) + __vsadu4(__vabsss4(q.z), 0) +
+                           __vsadu4(__vabsss4(q.w), 0));
+            }
             fw.l1[r] = valid[r] ? s : -1;
         }
     }
 }
 
-__global__ void hist_kernel(const int32_t* l1, int64_t count, int32_t* hist) {
+// L1 histogram with block-local (shared-memory) aggregation: one global atomic per bin per block
+__global__ void hist_kernel(const int32_t* l1, int64_t count, int32_t* hist, int nb) {
+    extern __shared__ int32_t sh_hist[];
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) sh_hist[i] = 0;
+    __syncthreads();
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
-        if (l1[r] >= 0) atomicAdd(&hist[l1[r]], 1);
+        if (l1[r] >= 0) atomicAdd(&sh_hist[l1[r]], 1);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nb; i += blockDim.x)
+        if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
 }
 
 // exclusive scan of hist[0..nb) -> start[0..nb], single block
@@ -164,9 +185,33 @@ __global__ void scan_kernel(const int32_t* hist, int nb, int32_t* start, int32_t
     }
 }
 
-__global__ void scatter_kernel(const int32_t* l1, int64_t count, int32_t* cursor, int32_t* order) {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
-        if (l1[r] >= 0) order[atomicAdd(&cursor[l1[r]], 1)] = (int32_t)r;
+// bucket scatter: each block counts its rows per bin, reserves one contiguous range per bin with a single
+// global atomic, then places its rows (the order inside a bucket is irrelevant to the filter's result)
+__global__ void scatter_kernel(const int32_t* l1, int64_t count, int32_t* cursor, int32_t* order, int nb) {
+    extern __shared__ int32_t sh[];
+    int32_t* cnt = sh;
+    int32_t* base = sh + nb;
+    const int64_t chunk = (int64_t)blockDim.x * 8;
+    for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < count; c0 += (int64_t)gridDim.x * chunk) {
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
+        __syncthreads();
+        int lv[8], slot[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t r = c0 + k * blockDim.x + threadIdx.x;
+            lv[k] = r < count ? l1[r] : -1;
+            slot[k] = lv[k] >= 0 ? atomicAdd(&cnt[lv[k]], 1) : 0;
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) base[i] = cnt[i] ? atomicAdd(&cursor[i], cnt[i]) : 0;
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t r = c0 + k * blockDim.x + threadIdx.x;
+            if (lv[k] >= 0) order[base[lv[k]] + slot[k]] = (int32_t)r;
+        }
+        __syncthreads();
+    }
 }
 
 constexpr int kFilterThreads = 256;
@@ -346,13 +391,13 @@ cudaError_t launch_dedupe(const int8_t* rows, int64_t count, int row_stride, int
 cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& cp, uint8_t* flags,
                          unsigned long long* n_bad, cudaStream_t s) {
     if (count <= 0) return cudaSuccess;
-    const size_t smem = (size_t)(cp.m + 1 + 2 * cp.nnz) * 4;
-    const int smem_ok = smem <= 160 * 1024;
-    if (smem_ok && smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    check_kernel<<<grid_for(count), 256, smem_ok ? smem : 0, s>>>(rows, count, cp, flags, n_bad, smem_ok);
+    const size_t smem = (size_t)(((cp.m + 1 + 2 * cp.nnz + cp.n) + 3) & ~3) * 4 + (size_t)kCheckThreads * cp.n_pad;
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (count + kCheckThreads - 1) / kCheckThreads;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    check_kernel<<<(unsigned)blocks, kCheckThreads, smem, s>>>(rows, count, cp, flags, n_bad);
     return cudaGetLastError();
 }
 
@@ -367,9 +412,11 @@ cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t coun
     cudaError_t e;
     codes_kernel<<<grid_for(count * 2 * fw.Wh), 256, 0, s>>>(rows, valid, count, fw);
     if ((e = cudaMemsetAsync(fw.hist, 0, sizeof(int32_t) * (fw.Lmax + 2), s)) != cudaSuccess) return e;
-    hist_kernel<<<grid_for(count), 256, 0, s>>>(fw.l1, count, fw.hist);
-    scan_kernel<<<1, 32, 0, s>>>(fw.hist, fw.Lmax + 1, fw.level_start, fw.cursor);
-    scatter_kernel<<<grid_for(count), 256, 0, s>>>(fw.l1, count, fw.cursor, fw.order);
+    const int nb = fw.Lmax + 1;
+    hist_kernel<<<std::min<unsigned>(grid_for(count), 148 * 4), 256, nb * 4, s>>>(fw.l1, count, fw.hist, nb);
+    scan_kernel<<<1, 32, 0, s>>>(fw.hist, nb, fw.level_start, fw.cursor);
+    scatter_kernel<<<std::min<unsigned>(grid_for((count + 7) / 8), 148 * 4), 256, 2 * nb * 4, s>>>(
+        fw.l1, count, fw.cursor, fw.order, nb);
     *launches += 4;
     // number of valid rows = level_start[Lmax + 1]; read on host to size the grid
     int32_t n_valid = 0;

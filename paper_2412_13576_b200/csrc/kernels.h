@@ -9,7 +9,7 @@ struct DescentParams {
     int n, d, n_pad, T;
     float lam1, lam2, beta1, beta2, eps;
     float omb1, omb2;             // (1 - beta1), (1 - beta2) rounded from fp64 (torch.optim.Adam scalars)
-    const float2* step_tab;       // per step t=1..T: (lr / (1 - beta1^t), sqrt(1 - beta2^t)) as fp32
+    const float4* step_tab;       // per step t=1..T: (lr/(1-beta1^t), sqrt(1-beta2^t), 1/sqrt(1-beta2^t), 0)
     uint64_t seed;
     int64_t n_total;              // RNG key space (global start count)
     int64_t begin, count;         // global starts [begin, begin + count)
@@ -67,8 +67,9 @@ cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& c
 struct FilterWork {
     int n, n_pad;
     int Lh, Wh;                   // thermometer bits per half, 32-bit words per half
-    const int32_t* bit_coord;     // Lh: coordinate of each thermometer bit
-    const int32_t* bit_k;         // Lh: threshold k >= 1 of each bit
+    const int32_t* off;           // n: first thermometer bit of coordinate i (prefix sum of u - l)
+    const int32_t* word_c0;       // Wh: first coordinate with a bit in word w
+    const int32_t* word_c1;       // Wh: last coordinate with a bit in word w
     uint32_t* codes;              // count x 2Wh
     int32_t* l1;                  // count
     int32_t* hist;                // Lmax + 2
@@ -95,6 +96,10 @@ struct AugmentParams {
     int n, m, n_pad;
     int n_dir;                    // canonical directions K; D = ±, sorted lexicographically: 2K entries
     const int8_t* dirs;           // D, 2K x n_pad (lex sorted, both signs)
+    const int32_t* nnz;           // ELL of D: nonzeros per row (2K)
+    const int16_t* col;           // 2K x nzmax column indices (ascending)
+    const int8_t* val;            // 2K x nzmax values
+    int nzmax;
     const double* Q;              // n x n (per instance: Q + inst * n * n)
     const double* c;              // n (per instance)
     const double* c0;             // per instance
@@ -109,6 +114,9 @@ struct AugmentParams {
 };
 cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s);
 cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s);
+// ELL form of the 2K rows of D (allocates *col, *val with cudaMalloc; *nzmax_host receives the width)
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax_dev,
+                               int16_t** col, int8_t** val, int* nzmax_host, cudaStream_t s);
 cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s);
 // D = rows ∪ -rows (2k rows, stride n_pad) written to out (unsorted; the caller lex-sorts it)
 cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t* out, cudaStream_t s);
