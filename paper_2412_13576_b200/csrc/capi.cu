@@ -19,21 +19,25 @@ using namespace maple;
 
 namespace {
 
+// Device workspace: stream-ordered allocations from the device's default memory pool (kept cached with a
+// maximal release threshold), so repeated contexts / calls do not pay cudaMalloc.
+thread_local cudaStream_t g_alloc_stream = 0;
+
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, g_alloc_stream);
         p = nullptr;
         bytes = 0;
         size_t b = std::max<size_t>(want, 256);
-        cudaError_t e = cudaMalloc(&p, b);
+        cudaError_t e = cudaMallocAsync(&p, b, g_alloc_stream);
         if (e == cudaSuccess) bytes = b;
         return e;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, g_alloc_stream);
         p = nullptr;
         bytes = 0;
     }
@@ -200,7 +204,7 @@ int finish_set(maple_ctx* ctx, int64_t pool_count, int filter_minimal, maple_dir
     CU(launch_check(ctx->pool.as<int8_t>(), K, cp, ctx->flags.as<uint8_t>(), counters(ctx) + C_BAD, s));
     if (K > 0) ctx->launches++;
     CU(cudaEventRecord(ctx->ev[3], s));
-    if (filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
                   ctx->th_c1.as<int32_t>(),
                   ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
@@ -401,6 +405,14 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     }
     if (cudaSetDevice(device) != cudaSuccess) return MAPLE_ERR_CUDA;
     ctx->device = device;
+    g_alloc_stream = 0;
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     for (auto& e : ctx->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return MAPLE_ERR_CUDA;
     // CSR of A
@@ -460,6 +472,7 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->th_c1, wc1));
     CU(ctx->counters.ensure(sizeof(unsigned long long) * C_N));
     CU(cudaMemset(ctx->counters.p, 0, sizeof(unsigned long long) * C_N));
+    CU(cudaDeviceSynchronize());
     *out = hold.release();
     return MAPLE_OK;
 }
@@ -487,6 +500,7 @@ void maple_destroy(maple_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    g_alloc_stream = ctx->stream;
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
@@ -495,6 +509,7 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,
                       &ctx->af2b};
     for (DevBuf* b : bufs) b->release();
+    cudaStreamSynchronize(ctx->stream);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -502,6 +517,7 @@ void maple_destroy(maple_ctx* ctx) {
 
 int maple_set_stream(maple_ctx* ctx, void* stream) {
     if (!ctx) return MAPLE_ERR_BAD_ARG;
+    cudaStreamSynchronize(ctx->stream);  // workspace allocated on the old stream is now safe to reuse
     ctx->stream = reinterpret_cast<cudaStream_t>(stream);
     return MAPLE_OK;
 }
@@ -579,10 +595,11 @@ int maple_last_timings(const maple_ctx* ctx, float* e6, float* a3) {
 
 int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
                         double step_size, uint64_t seed, maple_dirset** out) {
+    if (ctx) g_alloc_stream = ctx->stream;
     int rc = check_extract_args(ctx, n_starts, begin, end, steps, step_size);
     if (rc) return rc;
     if (!out) FAIL(MAPLE_ERR_BAD_ARG, "out is null");
-    if (ctx->filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    if (ctx->filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     CU(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     rc = build_step_table(ctx, steps, step_size);
@@ -674,16 +691,18 @@ int maple_extract(maple_ctx* ctx, int64_t n_starts, int32_t steps, double step_s
 }
 
 int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t stride, maple_dirset** out) {
+    if (ctx) g_alloc_stream = ctx->stream;
     if (!ctx || !out || k < 0 || (k > 0 && !rows) || stride < ctx->n) return MAPLE_ERR_BAD_ARG;
-    if (ctx->filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    if (ctx->filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     CU(cudaSetDevice(ctx->device));
     return insert_rows_and_finish(ctx, rows, k, stride, ctx->filter_minimal, out);
 }
 
 int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32_t filter_minimal,
                            maple_dirset** out) {
+    if (ctx) g_alloc_stream = ctx->stream;
     if (!ctx || !out || k < 0 || (k > 0 && !rows)) return MAPLE_ERR_BAD_ARG;
-    if (filter_minimal && ctx->Wh > 16) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 512");
+    if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     CU(cudaSetDevice(ctx->device));
     const int np = ctx->n_pad;
     std::vector<int8_t> h((size_t)std::max<int64_t>(k, 1) * np, 0);
@@ -750,6 +769,7 @@ int64_t maple_debug_candidates(maple_ctx* ctx, int32_t* host_rows, int64_t cap) 
 
 int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
                         double step_size, uint64_t seed, float* Z_out, double* Z0_out) {
+    if (ctx) g_alloc_stream = ctx->stream;
     int rc = check_extract_args(ctx, n_starts, begin, end, steps, step_size);
     if (rc) return rc;
     if (!Z_out) FAIL(MAPLE_ERR_BAD_ARG, "Z_out is null");
@@ -776,6 +796,7 @@ int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
 static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, const maple_objective* f,
                         const int32_t* b, const int32_t* x0, int32_t k0, int32_t* x_best, double* f_best,
                         int32_t* iters) {
+    if (ctx) g_alloc_stream = ctx->stream;
     const int n = ctx->n, m = ctx->m, np = ctx->n_pad;
     cudaStream_t s = ctx->stream;
     // exact feasibility of every incumbent

@@ -220,8 +220,9 @@ constexpr int kTile = 256;
 template <int WH>
 __global__ void __launch_bounds__(kFilterThreads)
 dominance_kernel(FilterWork fw, int32_t n_valid) {
-    __shared__ uint32_t tile[kTile * 2 * WH];
-    __shared__ int32_t tile_row[kTile];
+    extern __shared__ __align__(16) uint32_t dyn_sh[];
+    uint32_t* tile = dyn_sh;                                         // kTile x 2WH code words
+    int32_t* tile_row = reinterpret_cast<int32_t*>(dyn_sh + kTile * 2 * WH);
     const int Wh = fw.Wh;
     const int W2 = 2 * Wh;
     const int32_t pos = blockIdx.x * kFilterThreads + threadIdx.x;
@@ -427,12 +428,16 @@ cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t coun
     if ((e = cudaMemsetAsync(fw.keep, 0, count, s)) != cudaSuccess) return e;
     if (n_valid == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((n_valid + kFilterThreads - 1) / kFilterThreads);
-    if (fw.Wh <= 1) dominance_kernel<1><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
-    else if (fw.Wh <= 2) dominance_kernel<2><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
-    else if (fw.Wh <= 4) dominance_kernel<4><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
-    else if (fw.Wh <= 8) dominance_kernel<8><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
-    else if (fw.Wh <= 16) dominance_kernel<16><<<blocks, kFilterThreads, 0, s>>>(fw, n_valid);
-    else return cudaErrorInvalidValue;
+#define MAPLE_DOM(WHV)                                                                                       \
+    if (fw.Wh <= WHV) {                                                                                      \
+        const size_t sm = (size_t)kTile * (2 * WHV + 1) * 4;                                                 \
+        if ((e = cudaFuncSetAttribute(dominance_kernel<WHV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                      (int)sm)) != cudaSuccess)                                              \
+            return e;                                                                                        \
+        dominance_kernel<WHV><<<blocks, kFilterThreads, sm, s>>>(fw, n_valid);                              \
+    } else
+    MAPLE_DOM(1) MAPLE_DOM(2) MAPLE_DOM(4) MAPLE_DOM(8) MAPLE_DOM(16) MAPLE_DOM(32) return cudaErrorInvalidValue;
+#undef MAPLE_DOM
     *launches += 1;
     return cudaGetLastError();
 }
