@@ -73,7 +73,8 @@ struct maple_ctx {
     DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, l1, hist, level_start, cursor, order, keep,
         witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
     DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b;
-    int64_t cand_cap = 0, pool_cap = 0;
+    int64_t cand_cap = 0, pool_cap = 0, want_cand = 0, want_pool = 0;
+    bool timings_pending = false;
     uint64_t table_slots = 0;
     std::string err;
     float t_extract[6] = {0, 0, 0, 0, 0, 0};
@@ -82,7 +83,7 @@ struct maple_ctx {
     int debug_keep = 0;
     std::vector<int8_t> dbg_cand;
     int64_t dbg_count = 0;
-    cudaEvent_t ev[8] = {};
+    cudaEvent_t ev[12] = {};  // 0-5: extraction phases, 8-10: augmentation
 };
 
 struct maple_dirset {
@@ -98,7 +99,7 @@ struct maple_dirset {
 };
 
 // counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
-enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_N = 6 };
+enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_N = 6 };
 
 #define FAIL(code, msg)              \
     do {                             \
@@ -134,99 +135,90 @@ int read_counters(maple_ctx* ctx, unsigned long long* h) {
     return MAPLE_OK;
 }
 
-// (Re)build an empty hash set able to hold `cap` unique rows; existing pool rows are re-inserted.
-int ensure_set(maple_ctx* ctx, int64_t cap, bool keep_existing, int64_t existing) {
-    if (cap <= ctx->pool_cap) {
-        if (!keep_existing) {
-            CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
-            CU(cudaMemsetAsync(ctx->idx.p, 0xFF, ctx->table_slots * 4, ctx->stream));
-            CU(cudaMemsetAsync(counters(ctx) + C_POOL, 0, 8, ctx->stream));
-        }
-        return MAPLE_OK;
+// Size the candidate buffer, the hash set (pool + table) and the per-row work buffers, then reset the set.
+int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
+    const int np = ctx->n_pad;
+    if (cand_cap > ctx->cand_cap) {
+        ctx->cand.release();
+        CU(ctx->cand.ensure((size_t)cand_cap * np));
+        ctx->cand_cap = cand_cap;
     }
-    int64_t newcap = std::max<int64_t>(cap, std::max<int64_t>(4096, ctx->pool_cap * 2));
-    uint64_t slots = next_pow2((uint64_t)newcap * 2);
-    DevBuf newpool;
-    CU(newpool.ensure((size_t)newcap * ctx->n_pad));
-    if (keep_existing && existing > 0)
-        CU(cudaMemcpyAsync(newpool.p, ctx->pool.p, (size_t)existing * ctx->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    ctx->pool.release();
-    ctx->pool = newpool;
-    newpool.p = nullptr;
-    CU(ctx->keys.ensure(slots * 8));
-    CU(ctx->idx.ensure(slots * 4));
-    ctx->table_slots = slots;
-    ctx->pool_cap = newcap;
-    CU(cudaMemsetAsync(ctx->keys.p, 0, slots * 8, ctx->stream));
-    CU(cudaMemsetAsync(ctx->idx.p, 0xFF, slots * 4, ctx->stream));
-    CU(cudaMemsetAsync(counters(ctx) + C_POOL, 0, 8, ctx->stream));
-    if (keep_existing && existing > 0) {
-        // re-insert the existing unique rows into the new table (they stay at the front of the pool)
-        DevBuf tmp;
-        CU(tmp.ensure((size_t)existing * ctx->n_pad));
-        CU(cudaMemcpyAsync(tmp.p, ctx->pool.p, (size_t)existing * ctx->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
-        HashSet hs{ctx->keys.as<unsigned long long>(), ctx->idx.as<int32_t>(), slots - 1, ctx->pool.as<int8_t>(),
-                   ctx->pool_cap, counters(ctx) + C_POOL, reinterpret_cast<int*>(counters(ctx) + C_OVF)};
-        CU(launch_dedupe(tmp.as<int8_t>(), existing, ctx->n_pad, ctx->n_pad, hs, ctx->stream));
-        ctx->launches++;
-        CU(cudaStreamSynchronize(ctx->stream));
-        tmp.release();
+    if (pool_cap > ctx->pool_cap) {
+        const uint64_t slots = next_pow2((uint64_t)pool_cap * 2);
+        ctx->pool.release();
+        ctx->keys.release();
+        ctx->idx.release();
+        CU(ctx->pool.ensure((size_t)pool_cap * np));
+        CU(ctx->keys.ensure(slots * 8));
+        CU(ctx->idx.ensure(slots * 4));
+        ctx->table_slots = slots;
+        ctx->pool_cap = pool_cap;
+        const int64_t K = pool_cap;
+        CU(ctx->flags.ensure(K));
+        CU(ctx->keep.ensure(K));
+        CU(ctx->witness.ensure(K * 4));
+        CU(ctx->order.ensure(K * 4));
+        CU(ctx->l1.ensure(K * 4));
+        CU(ctx->codes.ensure((size_t)K * 2 * std::max(ctx->Wh, 1) * 4));
+        CU(ctx->tmp_rows.ensure((size_t)K * np));
     }
+    CU(ctx->hist.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(ctx->level_start.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(ctx->cursor.ensure((size_t)(ctx->Lh + 2) * 4));
+    CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
+    CU(cudaMemsetAsync(ctx->idx.p, 0xFF, ctx->table_slots * 4, ctx->stream));
+    CU(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_N, ctx->stream));
     return MAPLE_OK;
 }
 
 HashSet hashset(maple_ctx* ctx) {
     return HashSet{ctx->keys.as<unsigned long long>(), ctx->idx.as<int32_t>(), ctx->table_slots - 1,
                    ctx->pool.as<int8_t>(), ctx->pool_cap, counters(ctx) + C_POOL,
-                   reinterpret_cast<int*>(counters(ctx) + C_OVF)};
+                   reinterpret_cast<int*>(counters(ctx) + C_OVF), counters(ctx) + C_MAXC};
 }
 
-// check -> filter -> compact -> lex sort of the ctx pool (pool_count rows) into a new dirset
-int finish_set(maple_ctx* ctx, int64_t pool_count, int filter_minimal, maple_dirset** out) {
+// check -> filter -> compact of the ctx pool (device count) -> ONE host sync -> lex sort into a new dirset.
+// Returns MAPLE_OK, or RETRY (1) when a candidate / pool buffer overflowed (the caller grows and redoes).
+constexpr int RETRY = 1;
+int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     cudaStream_t s = ctx->stream;
     const int np = ctx->n_pad;
-    const int64_t K = pool_count;
-    CU(ctx->flags.ensure(std::max<int64_t>(K, 1)));
-    CU(ctx->keep.ensure(std::max<int64_t>(K, 1)));
-    CU(ctx->witness.ensure(std::max<int64_t>(K, 1) * 4));
-    CU(ctx->order.ensure(std::max<int64_t>(K, 1) * 4));
-    CU(ctx->l1.ensure(std::max<int64_t>(K, 1) * 4));
-    CU(ctx->codes.ensure(std::max<int64_t>(K, 1) * 2 * std::max(ctx->Wh, 1) * 4));
-    CU(ctx->hist.ensure((size_t)(ctx->Lh + 2) * 4));
-    CU(ctx->level_start.ensure((size_t)(ctx->Lh + 2) * 4));
-    CU(ctx->cursor.ensure((size_t)(ctx->Lh + 2) * 4));
-    CU(ctx->tmp_rows.ensure(std::max<int64_t>(K, 1) * np));
+    const int64_t K = ctx->pool_cap;
     CU(cudaEventRecord(ctx->ev[2], s));
     CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
                    ctx->nnz, ctx->dbox.as<int32_t>()};
-    CU(cudaMemsetAsync(counters(ctx) + C_BAD, 0, 16, s));
-    CU(launch_check(ctx->pool.as<int8_t>(), K, cp, ctx->flags.as<uint8_t>(), counters(ctx) + C_BAD, s));
-    if (K > 0) ctx->launches++;
-    CU(cudaEventRecord(ctx->ev[3], s));
     if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
-                  ctx->th_c1.as<int32_t>(),
-                  ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
+                  ctx->th_c1.as<int32_t>(), ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
                   ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh};
+    const unsigned long long* dpool = counters(ctx) + C_POOL;
+    CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, filter_minimal, ctx->flags.as<uint8_t>(),
+                          counters(ctx) + C_BAD, s));
+    ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[3], s));
     int nl = 0;
-    CU(launch_filter(ctx->pool.as<int8_t>(), ctx->flags.as<uint8_t>(), K, fw, filter_minimal, s, &nl));
+    CU(launch_filter(dpool, K, ctx->flags.as<uint8_t>(), fw, filter_minimal, s, &nl));
     ctx->launches += nl;
-    CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), K, np, ctx->tmp_rows.as<int8_t>(),
+    CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), dpool, K, np, ctx->tmp_rows.as<int8_t>(),
                       counters(ctx) + C_KEEP, s));
-    if (K > 0) ctx->launches++;
+    ctx->launches++;
     CU(cudaEventRecord(ctx->ev[4], s));
     unsigned long long h[C_N];
     int rc = read_counters(ctx, h);
     if (rc) return rc;
+    if (h[C_OVF] || (int64_t)h[C_MAXC] > ctx->cand_cap) {
+        ctx->want_cand = std::max<int64_t>(ctx->cand_cap, (int64_t)h[C_MAXC] + ((int64_t)h[C_MAXC] >> 2) + 1024);
+        ctx->want_pool = h[C_OVF] ? 2 * ctx->pool_cap : ctx->pool_cap;
+        return RETRY;
+    }
     const int64_t M = (int64_t)h[C_KEEP];
     maple_dirset* ds = new maple_dirset();
     ds->ctx = ctx;
     ds->n = ctx->n;
     ds->n_pad = np;
     ds->size = M;
-    ds->pool_size = K - (int64_t)h[C_BAD];
+    ds->pool_size = (int64_t)h[C_POOL] - (int64_t)h[C_BAD];
     ds->n_bad = (int64_t)h[C_BAD];
     cudaError_t e = cudaMalloc(&ds->rows, std::max<int64_t>(M, 1) * np);
     if (e != cudaSuccess) {
@@ -241,7 +233,7 @@ int finish_set(maple_ctx* ctx, int64_t pool_count, int filter_minimal, maple_dir
                        ctx->sidx1.as<int32_t>(), ds->rows, s, &nl));
     ctx->launches += nl;
     CU(cudaEventRecord(ctx->ev[5], s));
-    CU(cudaStreamSynchronize(s));
+    ctx->timings_pending = true;
     *out = ds;
     return MAPLE_OK;
 }
@@ -261,39 +253,26 @@ __global__ void canonical_copy_kernel(const int8_t* __restrict__ rows, int64_t k
 int insert_rows_and_finish(maple_ctx* ctx, const int8_t* drows, int64_t k, int stride, int filter_minimal,
                            maple_dirset** out) {
     cudaStream_t s = ctx->stream;
-    CU(cudaEventRecord(ctx->ev[0], s));
-    CU(cudaEventRecord(ctx->ev[1], s));
-    CU(ctx->cand.ensure(std::max<int64_t>(k, 1) * ctx->n_pad));
-    if (k > 0) {
-        unsigned blocks = (unsigned)std::min<int64_t>((k + 255) / 256, 148 * 16);
-        canonical_copy_kernel<<<blocks, 256, 0, s>>>(drows, k, stride, ctx->n, ctx->n_pad, ctx->cand.as<int8_t>());
-        CU(cudaGetLastError());
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        int rc = prepare_set(ctx, std::max<int64_t>(k, 1), std::max<int64_t>({k, ctx->want_pool, 1}));
+        if (rc) return rc;
+        CU(cudaEventRecord(ctx->ev[0], s));
+        const unsigned long long kk = (unsigned long long)k;
+        CU(cudaMemcpyAsync(counters(ctx) + C_CAND, &kk, sizeof(kk), cudaMemcpyHostToDevice, s));
+        if (k > 0) {
+            unsigned blocks = (unsigned)std::min<int64_t>((k + 255) / 256, 148 * 16);
+            canonical_copy_kernel<<<blocks, 256, 0, s>>>(drows, k, stride, ctx->n, ctx->n_pad, ctx->cand.as<int8_t>());
+            CU(cudaGetLastError());
+            ctx->launches++;
+        }
+        CU(cudaEventRecord(ctx->ev[1], s));
+        CU(launch_dedupe(ctx->cand.as<int8_t>(), counters(ctx) + C_CAND, ctx->cand_cap, ctx->n_pad, ctx->n_pad,
+                         hashset(ctx), s));
         ctx->launches++;
+        rc = finish_set(ctx, filter_minimal, out);
+        if (rc != RETRY) return rc;
     }
-    int rc = ensure_set(ctx, std::max<int64_t>(k, 1), false, 0);
-    if (rc) return rc;
-    CU(cudaMemsetAsync(counters(ctx) + C_OVF, 0, 8, s));
-    CU(launch_dedupe(ctx->cand.as<int8_t>(), k, ctx->n_pad, ctx->n_pad, hashset(ctx), s));
-    if (k > 0) ctx->launches++;
-    unsigned long long h[C_N];
-    rc = read_counters(ctx, h);
-    if (rc) return rc;
-    if (h[C_OVF]) FAIL(MAPLE_ERR_CAPACITY, "hash set overflow");
-    rc = finish_set(ctx, (int64_t)h[C_POOL], filter_minimal, out);
-    if (rc) return rc;
-    float t;
-    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
-    ctx->t_extract[1] = t;
-    cudaEventElapsedTime(&t, ctx->ev[2], ctx->ev[3]);
-    ctx->t_extract[2] = t;
-    cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
-    ctx->t_extract[3] = t;
-    cudaEventElapsedTime(&t, ctx->ev[4], ctx->ev[5]);
-    ctx->t_extract[4] = t;
-    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[5]);
-    ctx->t_extract[5] = t;
-    ctx->t_extract[0] = 0;
-    return MAPLE_OK;
+    FAIL(MAPLE_ERR_CAPACITY, "device set capacity retries exhausted");
 }
 
 int build_step_table(maple_ctx* ctx, int T, double lr) {
@@ -586,8 +565,22 @@ int32_t maple_dim_d(const maple_ctx* ctx) { return ctx ? ctx->d : -1; }
 const char* maple_last_error(const maple_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 int64_t maple_kernel_launches(const maple_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
-int maple_last_timings(const maple_ctx* ctx, float* e6, float* a3) {
+int maple_last_timings(const maple_ctx* ctx_c, float* e6, float* a3) {
+    maple_ctx* ctx = const_cast<maple_ctx*>(ctx_c);
     if (!ctx) return MAPLE_ERR_BAD_ARG;
+    if (ctx->timings_pending) {
+        // events: 0 start, 1 descent done, 2 dedupe done, 3 check done, 4 filter + compact done, 5 sorted
+        CU(cudaEventSynchronize(ctx->ev[5]));
+        float t[5];
+        cudaEventElapsedTime(&t[0], ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&t[1], ctx->ev[1], ctx->ev[2]);
+        cudaEventElapsedTime(&t[2], ctx->ev[2], ctx->ev[3]);
+        cudaEventElapsedTime(&t[3], ctx->ev[3], ctx->ev[4]);
+        cudaEventElapsedTime(&t[4], ctx->ev[4], ctx->ev[5]);
+        for (int i = 0; i < 5; ++i) ctx->t_extract[i] = t[i];
+        cudaEventElapsedTime(&ctx->t_extract[5], ctx->ev[0], ctx->ev[5]);
+        ctx->timings_pending = false;
+    }
     if (e6) std::memcpy(e6, ctx->t_extract, sizeof(ctx->t_extract));
     if (a3) std::memcpy(a3, ctx->t_augment, sizeof(ctx->t_augment));
     return MAPLE_OK;
@@ -605,84 +598,48 @@ int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
     rc = build_step_table(ctx, steps, step_size);
     if (rc) return rc;
     const int np = ctx->n_pad;
+    const int64_t total = end - begin;
     const int64_t chunk_max = 1 << 18;
-    if (ctx->cand_cap == 0) {
-        const int64_t want = std::min<int64_t>((int64_t)std::max<int64_t>(end - begin, 1) * 8, (int64_t)1 << 22);
-        CU(ctx->cand.ensure((size_t)want * np));
-        ctx->cand_cap = want;
-    }
-    rc = ensure_set(ctx, std::max<int64_t>(ctx->pool_cap, 4096), false, 0);
-    if (rc) return rc;
-    ctx->dbg_cand.clear();
-    ctx->dbg_count = 0;
-    float t_desc = 0.f, t_dd = 0.f;
-    CU(cudaEventRecord(ctx->ev[0], s));
-    int64_t pool_now = 0;
-    for (int64_t c0 = begin; c0 < end;) {
-        const int64_t cnt = std::min(chunk_max, end - c0);
-        unsigned long long h[C_N];
-        for (;;) {
+    const int64_t nchunks = std::max<int64_t>(1, (total + chunk_max - 1) / chunk_max);
+    const int64_t per_chunk = std::min(total, chunk_max);
+    // initial capacities (grown on overflow): ~32 candidate rows per start per chunk; the unique pool can
+    // never exceed the candidates of one chunk times the number of chunks
+    if (ctx->want_cand < per_chunk * 32) ctx->want_cand = std::max<int64_t>(per_chunk * 32, 4096);
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        const int64_t pool_want = std::max<int64_t>(ctx->want_pool, std::max(ctx->want_cand, ctx->cand_cap) *
+                                                                         std::min<int64_t>(nchunks, 4));
+        rc = prepare_set(ctx, std::max(ctx->want_cand, ctx->cand_cap), pool_want);
+        if (rc) return rc;
+        ctx->dbg_cand.clear();
+        ctx->dbg_count = 0;
+        CU(cudaEventRecord(ctx->ev[0], s));
+        for (int64_t c0 = begin; c0 < end; c0 += chunk_max) {
+            const int64_t cnt = std::min(chunk_max, end - c0);
             CU(cudaMemsetAsync(counters(ctx) + C_CAND, 0, 8, s));
             DescentParams p = descent_params(ctx, steps, seed, n_starts, c0, cnt);
             p.harvest = 1;
             p.cand = ctx->cand.as<int8_t>();
             p.cand_cap = ctx->cand_cap;
             p.cand_count = counters(ctx) + C_CAND;
-            CU(cudaEventRecord(ctx->ev[6], s));
             CU(run_descent(ctx, p));
-            CU(cudaEventRecord(ctx->ev[7], s));
-            rc = read_counters(ctx, h);
-            if (rc) return rc;
-            float t;
-            cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
-            t_desc += t;
-            if ((int64_t)h[C_CAND] <= ctx->cand_cap) break;
-            // the candidate buffer was too small: grow to the exact count and recompute this chunk
-            const int64_t want = (int64_t)h[C_CAND] + ((int64_t)h[C_CAND] >> 3) + 1024;
-            ctx->cand.release();
-            CU(ctx->cand.ensure((size_t)want * np));
-            ctx->cand_cap = want;
+            if (c0 + chunk_max >= end) CU(cudaEventRecord(ctx->ev[1], s));
+            if (ctx->debug_keep) {
+                unsigned long long h[C_N];
+                rc = read_counters(ctx, h);
+                if (rc) return rc;
+                const int64_t nc = std::min<int64_t>((int64_t)h[C_CAND], ctx->cand_cap);
+                const size_t off = ctx->dbg_cand.size();
+                ctx->dbg_cand.resize(off + (size_t)nc * np);
+                if (nc) CU(cudaMemcpy(ctx->dbg_cand.data() + off, ctx->cand.p, (size_t)nc * np, cudaMemcpyDeviceToHost));
+                ctx->dbg_count += nc;
+            }
+            CU(launch_dedupe(ctx->cand.as<int8_t>(), counters(ctx) + C_CAND, ctx->cand_cap, np, np, hashset(ctx), s));
+            ctx->launches++;
         }
-        const int64_t nc = (int64_t)h[C_CAND];
-        if (ctx->debug_keep && nc > 0) {
-            const size_t off = ctx->dbg_cand.size();
-            ctx->dbg_cand.resize(off + (size_t)nc * np);
-            CU(cudaMemcpy(ctx->dbg_cand.data() + off, ctx->cand.p, (size_t)nc * np, cudaMemcpyDeviceToHost));
-            ctx->dbg_count += nc;
-        }
-        if (pool_now + nc > ctx->pool_cap) {
-            rc = ensure_set(ctx, pool_now + nc, true, pool_now);
-            if (rc) return rc;
-        }
-        CU(cudaEventRecord(ctx->ev[6], s));
-        CU(cudaMemsetAsync(counters(ctx) + C_OVF, 0, 8, s));
-        CU(launch_dedupe(ctx->cand.as<int8_t>(), nc, np, np, hashset(ctx), s));
-        if (nc > 0) ctx->launches++;
-        CU(cudaEventRecord(ctx->ev[7], s));
-        rc = read_counters(ctx, h);
-        if (rc) return rc;
-        float t;
-        cudaEventElapsedTime(&t, ctx->ev[6], ctx->ev[7]);
-        t_dd += t;
-        if (h[C_OVF]) FAIL(MAPLE_ERR_CAPACITY, "hash set overflow");
-        pool_now = (int64_t)h[C_POOL];
-        c0 += cnt;
+        rc = finish_set(ctx, ctx->filter_minimal, out);
+        if (rc != RETRY) return rc;
     }
-    CU(cudaEventRecord(ctx->ev[1], s));
-    rc = finish_set(ctx, pool_now, ctx->filter_minimal, out);
-    if (rc) return rc;
-    float t;
-    ctx->t_extract[0] = t_desc;
-    ctx->t_extract[1] = t_dd;
-    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[3]);
-    ctx->t_extract[2] = t;
-    cudaEventElapsedTime(&t, ctx->ev[3], ctx->ev[4]);
-    ctx->t_extract[3] = t;
-    cudaEventElapsedTime(&t, ctx->ev[4], ctx->ev[5]);
-    ctx->t_extract[4] = t;
-    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[5]);
-    ctx->t_extract[5] = t;
-    return MAPLE_OK;
+    FAIL(MAPLE_ERR_CAPACITY, "device set capacity retries exhausted");
 }
 
 int maple_extract(maple_ctx* ctx, int64_t n_starts, int32_t steps, double step_size, uint64_t seed,
@@ -814,7 +771,7 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     for (int t = 0; t < n_inst; ++t)
         if (!f[t].c || !f[t].Q || (f[t].kind != MAPLE_OBJ_QUADRATIC && f[t].kind != MAPLE_OBJ_SEPARABLE))
             FAIL(MAPLE_ERR_BAD_ARG, "bad objective");
-    CU(cudaEventRecord(ctx->ev[0], s));
+    CU(cudaEventRecord(ctx->ev[8], s));
     maple_dirset* dsm = const_cast<maple_dirset*>(ds);
     const int64_t K = ds->size;
     if (!dsm->D && K > 0) {
@@ -894,11 +851,11 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     p.max_iter = 1 << 20;
     CU(launch_augment_qg(p, s));
     ctx->launches++;
-    CU(cudaEventRecord(ctx->ev[1], s));
+    CU(cudaEventRecord(ctx->ev[9], s));
     CU(launch_augment(p, s));
     CU(launch_augment_best(p, ctx->axb.as<int32_t>(), ctx->af2b.as<double>(), s));
     ctx->launches += 2;
-    CU(cudaEventRecord(ctx->ev[2], s));
+    CU(cudaEventRecord(ctx->ev[10], s));
     std::vector<double> f2(n_inst);
     CU(cudaMemcpyAsync(x_best, ctx->axb.p, (size_t)n_inst * n * 4, cudaMemcpyDeviceToHost, s));
     CU(cudaMemcpyAsync(f2.data(), ctx->af2b.p, (size_t)n_inst * 8, cudaMemcpyDeviceToHost, s));
@@ -906,11 +863,11 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     CU(cudaStreamSynchronize(s));
     for (int t = 0; t < n_inst; ++t) f_best[t] = f2[t] / 2.0;
     float t;
-    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[1]);
+    cudaEventElapsedTime(&t, ctx->ev[8], ctx->ev[9]);
     ctx->t_augment[0] = t;
-    cudaEventElapsedTime(&t, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&t, ctx->ev[9], ctx->ev[10]);
     ctx->t_augment[1] = t;
-    cudaEventElapsedTime(&t, ctx->ev[0], ctx->ev[2]);
+    cudaEventElapsedTime(&t, ctx->ev[8], ctx->ev[10]);
     ctx->t_augment[2] = t;
     return MAPLE_OK;
 }

@@ -178,35 +178,49 @@ augment_kernel(AugmentParams p) {
     }
 }
 
-__device__ __forceinline__ bool inc_better(const AugmentParams& p, int a, int b) {
+__device__ __forceinline__ bool inc_better(const double* F2, const int32_t* X, int n, int a, int b) {
     if (b < 0) return a >= 0;
     if (a < 0) return false;
-    const double fa = p.F2[a], fb = p.F2[b];
+    const double fa = F2[a], fb = F2[b];
     if (fa != fb) return fa < fb;
-    const int32_t* xa = p.X + (size_t)a * p.n;
-    const int32_t* xb = p.X + (size_t)b * p.n;
-    for (int i = 0; i < p.n; ++i)
+    const int32_t* xa = X + (size_t)a * n;
+    const int32_t* xb = X + (size_t)b * n;
+    for (int i = 0; i < n; ++i)
         if (xa[i] != xb[i]) return xa[i] < xb[i];
     return a < b;
 }
 
-// per instance (one block): the best final incumbent (min 2f, ties lexicographically smallest x; reading #19)
-__global__ void best_kernel(AugmentParams p, int32_t* xbest, double* f2best) {
+// per instance (one block): the best final incumbent (min 2f, ties lexicographically smallest x; reading #19).
+// The instance's incumbents are staged in shared memory when they fit (dynamic smem = k0 * (n*4 + 8) bytes).
+__global__ void best_kernel(AugmentParams p, int32_t* xbest, double* f2best, int staged) {
+    extern __shared__ __align__(16) unsigned char bsm[];
     __shared__ int cand[128];
     const int inst = blockIdx.x;
     const int base = inst * p.k0;
+    const double* F2 = p.F2 + base;
+    const int32_t* X = p.X + (size_t)base * p.n;
+    if (staged) {
+        double* sF = reinterpret_cast<double*>(bsm);
+        int32_t* sX = reinterpret_cast<int32_t*>(sF + p.k0);
+        for (int k = threadIdx.x; k < p.k0; k += blockDim.x) sF[k] = F2[k];
+        for (int e = threadIdx.x; e < p.k0 * p.n; e += blockDim.x) sX[e] = X[e];
+        __syncthreads();
+        F2 = sF;
+        X = sX;
+    }
     int b = -1;
     for (int k = threadIdx.x; k < p.k0; k += blockDim.x)
-        if (inc_better(p, base + k, b)) b = base + k;
+        if (inc_better(F2, X, p.n, k, b)) b = k;
     cand[threadIdx.x] = b;
     __syncthreads();
     for (int w = 64; w > 0; w >>= 1) {
-        if (threadIdx.x < w && inc_better(p, cand[threadIdx.x + w], cand[threadIdx.x])) cand[threadIdx.x] = cand[threadIdx.x + w];
+        if (threadIdx.x < w && inc_better(F2, X, p.n, cand[threadIdx.x + w], cand[threadIdx.x]))
+            cand[threadIdx.x] = cand[threadIdx.x + w];
         __syncthreads();
     }
     const int bb = cand[0];
-    for (int i = threadIdx.x; i < p.n; i += blockDim.x) xbest[(size_t)inst * p.n + i] = p.X[(size_t)bb * p.n + i];
-    if (threadIdx.x == 0) f2best[inst] = p.F2[bb];
+    for (int i = threadIdx.x; i < p.n; i += blockDim.x) xbest[(size_t)inst * p.n + i] = X[(size_t)bb * p.n + i];
+    if (threadIdx.x == 0) f2best[inst] = F2[bb];
 }
 
 }  // namespace
@@ -233,7 +247,13 @@ cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int
 
 cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s) {
     if (p.n_inst <= 0 || p.k0 <= 0) return cudaSuccess;
-    best_kernel<<<p.n_inst, 128, 0, s>>>(p, xbest, f2best);
+    const size_t smem = (size_t)p.k0 * ((size_t)p.n * 4 + 8);
+    const int staged = smem <= 160 * 1024;
+    if (staged && smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(best_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    best_kernel<<<p.n_inst, 128, staged ? smem : 0, s>>>(p, xbest, f2best, staged);
     return cudaGetLastError();
 }
 

@@ -1,10 +1,13 @@
 // North-star post-processing kernels: dedupe (+ sign twins), exact check, ⊑-minimal filter, compaction
 // and lexicographic sort. Rows are canonical int8 vectors (first nonzero > 0) with stride n_pad.
+// Every kernel takes its row count from device memory (the producer's counter), so the whole pipeline is
+// enqueued without host round trips; grids are sized from host upper bounds and loop grid-stride.
 //
 //  dedupe   open-addressing hash set over the whole row (64-bit key, full-row compare on a key hit):
 //           set semantics of Alg. 3's "𝒢 ∪ {·}"; sign twins were collapsed by canonicalisation.
-//  check    (C1)-(C3) of §4: A g = 0 in exact int64 (A as CSR in shared memory),
-//           g != 0, l - u <= g <= u - l.
+//           A plain load precedes the CAS so hot duplicate rows do not serialise on one atomic address.
+//  check    (C1)-(C3) of §4: A g = 0 in exact int64 (A as CSR in shared memory), g != 0,
+//           l - u <= g <= u - l; fused with the filter's encoding (thermometer code + L1 norm).
 //  filter   (C4) / Def. 1-2: g is dropped iff some other row h has h ⊑ g or h ⊑ -g.
 //           Rows are encoded as thermometer bitsets P = [g_i >= k], N = [g_i <= -k] (k = 1..u_i-l_i), so
 //           h ⊑ g  <=>  P_h ⊆ P_g and N_h ⊆ N_g,   h ⊑ -g  <=>  P_h ⊆ N_g and N_h ⊆ P_g.
@@ -20,6 +23,11 @@
 namespace maple {
 
 namespace {
+
+__device__ __forceinline__ int64_t dev_count(const unsigned long long* c, int64_t cap) {
+    const int64_t k = (int64_t)*c;
+    return k < cap ? k : cap;
+}
 
 __device__ __forceinline__ uint64_t row_hash(const int4* w, int nw) {
     uint64_t h = 0x243F6A8885A308D3ULL;
@@ -41,9 +49,11 @@ __device__ __forceinline__ bool rows_equal(const int4* a, const int4* b, int nw)
     return true;
 }
 
-__global__ void dedupe_kernel(const int8_t* __restrict__ rows, int64_t count, int row_stride, int n_pad,
-                              HashSet hs) {
+__global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned long long* dcount, int64_t cap,
+                              int row_stride, int n_pad, HashSet hs) {
     const int nw = n_pad / 16;
+    const int64_t count = dev_count(dcount, cap);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && hs.max_count) atomicMax(hs.max_count, *dcount);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count;
          r += (int64_t)gridDim.x * blockDim.x) {
         const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r * row_stride);
@@ -51,23 +61,26 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, int64_t count, in
         const unsigned long long key = (unsigned long long)(h | 1ULL);
         uint64_t pos = mix64(h ^ 0x9E3779B97F4A7C15ULL) & hs.mask;
         for (uint64_t probe = 0; probe <= hs.mask; ++probe) {
-            const unsigned long long prev = atomicCAS(&hs.keys[pos], 0ULL, key);
-            if (prev == 0ULL) {  // we own the slot: publish a new unique row
-                const unsigned long long idx = atomicAdd(hs.pool_count, 1ULL);
-                if ((int64_t)idx >= hs.pool_cap) {
-                    atomicExch(hs.overflow, 1);
-                    atomicExch(&hs.idx[pos], -2);
+            unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&hs.keys[pos]);
+            if (cur == 0ULL) {
+                cur = atomicCAS(&hs.keys[pos], 0ULL, key);
+                if (cur == 0ULL) {  // we own the slot: publish a new unique row
+                    const unsigned long long idx = atomicAdd(hs.pool_count, 1ULL);
+                    if ((int64_t)idx >= hs.pool_cap) {
+                        atomicExch(hs.overflow, 1);
+                        atomicExch(&hs.idx[pos], -2);
+                        break;
+                    }
+                    int4* dst = reinterpret_cast<int4*>(hs.pool + (size_t)idx * n_pad);
+                    for (int i = 0; i < nw; ++i) dst[i] = src[i];
+                    __threadfence();
+                    atomicExch(&hs.idx[pos], (int)idx);
                     break;
                 }
-                int4* dst = reinterpret_cast<int4*>(hs.pool + (size_t)idx * n_pad);
-                for (int i = 0; i < nw; ++i) dst[i] = src[i];
-                __threadfence();
-                atomicExch(&hs.idx[pos], (int)idx);
-                break;
             }
-            if (prev == key) {  // same key: wait for publication, then compare the full row
+            if (cur == key) {  // same key: wait for publication, then compare the full row
                 int idx;
-                while ((idx = atomicAdd(&hs.idx[pos], 0)) == -1) {
+                while ((idx = *reinterpret_cast<volatile int*>(&hs.idx[pos])) == -1) {
                 }
                 if (idx == -2) break;  // overflowed insert; reported via hs.overflow
                 __threadfence();
@@ -79,92 +92,94 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, int64_t count, in
     }
 }
 
-// (C1)-(C3): one thread per row; the block stages its rows in shared memory with coalesced 16-byte loads
-// (rows x n_pad bytes), A (CSR) sits in shared memory. Exact int64 accumulation of A g.
+// (C1)-(C3) + filter encoding, one thread per row. The block stages its rows in shared memory (coalesced
+// 16-byte loads, padded stride n_pad + 16); A (CSR), u - l and the thermometer offsets sit in shared memory.
 constexpr int kCheckThreads = 128;
-__global__ void __launch_bounds__(kCheckThreads) check_kernel(const int8_t* __restrict__ rows, int64_t count,
-                                                              CheckParams cp, uint8_t* flags, unsigned long long* n_bad) {
+__global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t* __restrict__ rows,
+                                                                   const unsigned long long* dcount, int64_t cap,
+                                                                   CheckParams cp, FilterWork fw, uint8_t* flags,
+                                                                   unsigned long long* n_bad, int encode) {
     extern __shared__ __align__(16) int32_t sh[];
     int32_t* srp = sh;
     int32_t* scol = srp + cp.m + 1;
     int32_t* sval = scol + cp.nnz;
     int32_t* sbox = sval + cp.nnz;
-    int8_t* srow = reinterpret_cast<int8_t*>(sh + (((cp.m + 1 + 2 * cp.nnz + cp.n) + 3) & ~3));
+    int32_t* soff = sbox + cp.n;
+    int32_t* swc0 = soff + cp.n;
+    int32_t* swc1 = swc0 + fw.Wh;
+    const int stride = cp.n_pad + 16;
+    int8_t* srow = reinterpret_cast<int8_t*>(sh + (((cp.m + 1 + 2 * cp.nnz + 2 * cp.n + 2 * fw.Wh) + 3) & ~3));
     for (int i = threadIdx.x; i <= cp.m; i += blockDim.x) srp[i] = cp.A_rowptr[i];
     for (int i = threadIdx.x; i < cp.nnz; i += blockDim.x) {
         scol[i] = cp.A_col[i];
         sval[i] = cp.A_val[i];
     }
-    for (int i = threadIdx.x; i < cp.n; i += blockDim.x) sbox[i] = cp.box[i];
+    for (int i = threadIdx.x; i < cp.n; i += blockDim.x) {
+        sbox[i] = cp.box[i];
+        soff[i] = fw.off[i];
+    }
+    for (int w = threadIdx.x; w < fw.Wh; w += blockDim.x) {
+        swc0[w] = fw.word_c0[w];
+        swc1[w] = fw.word_c1[w];
+    }
     const int nw = cp.n_pad / 16;
+    const int64_t count = dev_count(dcount, cap);
+    const int W2 = 2 * fw.Wh;
     unsigned long long bad = 0;
     for (int64_t r0 = (int64_t)blockIdx.x * kCheckThreads; r0 < count; r0 += (int64_t)gridDim.x * kCheckThreads) {
         __syncthreads();
         const int64_t nr = min((int64_t)kCheckThreads, count - r0);
         const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r0 * cp.n_pad);
-        for (int e = threadIdx.x; e < nr * nw; e += kCheckThreads) reinterpret_cast<int4*>(srow)[e] = src[e];
+        for (int e = threadIdx.x; e < nr * nw; e += kCheckThreads)
+            *reinterpret_cast<int4*>(srow + (e / nw) * stride + (e % nw) * 16) = src[e];
         __syncthreads();
-        if (threadIdx.x < nr) {
-            const int8_t* g = srow + threadIdx.x * cp.n_pad;
-            bool ok = true, nz = false;
-            for (int i = 0; i < cp.n; ++i) {
-                const int v = g[i];
-                nz |= (v != 0);
-                ok &= (abs(v) <= sbox[i]);
+        if (threadIdx.x >= nr) continue;
+        const int8_t* g = srow + threadIdx.x * stride;
+        bool ok = true, nz = false;
+        int l1 = 0;
+        for (int i = 0; i < cp.n; ++i) {
+            const int v = g[i];
+            nz |= (v != 0);
+            ok &= (abs(v) <= sbox[i]);
+            l1 += abs(v);
+        }
+        for (int a = 0; a < cp.m && ok; ++a) {
+            long long acc = 0;
+            for (int e = srp[a]; e < srp[a + 1]; ++e) acc += (long long)sval[e] * (long long)g[scol[e]];
+            ok &= (acc == 0);
+        }
+        ok &= nz;
+        const int64_t r = r0 + threadIdx.x;
+        flags[r] = ok ? 1 : 0;
+        bad += ok ? 0 : 1;
+        if (encode) {
+            fw.l1[r] = ok ? l1 : -1;
+            // thermometer code: coordinate i owns bits [off_i, off_i + u_i - l_i) of each half
+            uint32_t* code = fw.codes + (size_t)r * W2;
+            for (int hf = 0; hf < 2; ++hf) {
+                for (int w = 0; w < fw.Wh; ++w) {
+                    uint32_t word = 0;
+                    for (int i = swc0[w]; i <= swc1[w]; ++i) {
+                        const int v = hf ? -(int)g[i] : (int)g[i];   // bits [off_i, off_i + v) of this half
+                        if (v <= 0) continue;
+                        const int b0 = soff[i] - 32 * w, b1 = b0 + v;
+                        const int a = max(b0, 0), e = min(b1, 32);
+                        if (a < e) word |= (e - a == 32) ? 0xFFFFFFFFu : (((1u << (e - a)) - 1u) << a);
+                    }
+                    code[hf * fw.Wh + w] = word;
+                }
             }
-            for (int a = 0; a < cp.m && ok; ++a) {
-                long long acc = 0;
-                for (int e = srp[a]; e < srp[a + 1]; ++e) acc += (long long)sval[e] * (long long)g[scol[e]];
-                ok &= (acc == 0);
-            }
-            ok &= nz;
-            flags[r0 + threadIdx.x] = ok ? 1 : 0;
-            bad += ok ? 0 : 1;
         }
     }
     if (bad) atomicAdd(n_bad, bad);
 }
 
-// ---- filter ----
-// thermometer codes: thread per (row, word); word w of a half covers bits [32w, 32w+32), i.e. the coordinate
-// range [word_c0[w], word_c1[w]] (host precomputed), with bit offset off[i] = sum_{k<i} (u_k - l_k).
-__global__ void codes_kernel(const int8_t* __restrict__ rows, const uint8_t* valid, int64_t count, FilterWork fw) {
-    const int W2 = 2 * fw.Wh;
-    const int64_t total = count * W2;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = t / W2;
-        const int w = (int)(t % W2);
-        const bool neg = w >= fw.Wh;
-        const int wb = neg ? w - fw.Wh : w;
-        const int8_t* g = rows + (size_t)r * fw.n_pad;
-        uint32_t word = 0;
-        const int lo = wb * 32;
-        for (int i = fw.word_c0[wb]; i <= fw.word_c1[wb]; ++i) {
-            const int v = neg ? -(int)g[i] : (int)g[i];       // bits [off_i, off_i + v) are set
-            if (v <= 0) continue;
-            const int b0 = fw.off[i] - lo, b1 = b0 + v;          // relative to this word
-            const int a = max(b0, 0), e = min(b1, 32);
-            if (a < e) word |= (e - a == 32 ? 0xFFFFFFFFu : (((1u << (e - a)) - 1u) << a));
-        }
-        fw.codes[r * W2 + w] = word;
-        if (w == 0) {
-            int s = 0;
-            const int4* g4 = reinterpret_cast<const int4*>(g);
-            for (int c = 0; c < fw.n_pad / 16; ++c) {
-                const int4 q = g4[c];
-                s += (int)(__vsadu4(__vabsss4(q.x), 0) + __vsadu4(__vabsss4(q.y), 0) + __vsadu4(__vabsss4(q.z), 0) +
-                           __vsadu4(__vabsss4(q.w), 0));
-            }
-            fw.l1[r] = valid[r] ? s : -1;
-        }
-    }
-}
-
 // L1 histogram with block-local (shared-memory) aggregation: one global atomic per bin per block
-__global__ void hist_kernel(const int32_t* l1, int64_t count, int32_t* hist, int nb) {
+__global__ void hist_kernel(const int32_t* l1, const unsigned long long* dcount, int64_t cap, int32_t* hist, int nb) {
     extern __shared__ int32_t sh_hist[];
     for (int i = threadIdx.x; i < nb; i += blockDim.x) sh_hist[i] = 0;
     __syncthreads();
+    const int64_t count = dev_count(dcount, cap);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
         if (l1[r] >= 0) atomicAdd(&sh_hist[l1[r]], 1);
     __syncthreads();
@@ -172,7 +187,7 @@ __global__ void hist_kernel(const int32_t* l1, int64_t count, int32_t* hist, int
         if (sh_hist[i]) atomicAdd(&hist[i], sh_hist[i]);
 }
 
-// exclusive scan of hist[0..nb) -> start[0..nb], single block
+// exclusive scan of hist[0..nb) -> start[0..nb], single thread (nb <= 1025)
 __global__ void scan_kernel(const int32_t* hist, int nb, int32_t* start, int32_t* cursor) {
     if (threadIdx.x == 0) {
         int32_t acc = 0;
@@ -187,10 +202,12 @@ __global__ void scan_kernel(const int32_t* hist, int nb, int32_t* start, int32_t
 
 // bucket scatter: each block counts its rows per bin, reserves one contiguous range per bin with a single
 // global atomic, then places its rows (the order inside a bucket is irrelevant to the filter's result)
-__global__ void scatter_kernel(const int32_t* l1, int64_t count, int32_t* cursor, int32_t* order, int nb) {
+__global__ void scatter_kernel(const int32_t* l1, const unsigned long long* dcount, int64_t cap, int32_t* cursor,
+                               int32_t* order, int nb) {
     extern __shared__ int32_t sh[];
     int32_t* cnt = sh;
     int32_t* base = sh + nb;
+    const int64_t count = dev_count(dcount, cap);
     const int64_t chunk = (int64_t)blockDim.x * 8;
     for (int64_t c0 = (int64_t)blockIdx.x * chunk; c0 < count; c0 += (int64_t)gridDim.x * chunk) {
         for (int i = threadIdx.x; i < nb; i += blockDim.x) cnt[i] = 0;
@@ -217,85 +234,101 @@ __global__ void scatter_kernel(const int32_t* l1, int64_t count, int32_t* cursor
 constexpr int kFilterThreads = 256;
 constexpr int kTile = 256;
 
+// Dominance test. Rows are visited in L1 order (order[], level_start[]); a block takes 256 consecutive
+// positions and streams the candidate dominators (all rows of strictly smaller L1) through shared memory
+// tile by tile, each thread stopping at its first dominator; the block stops when all its rows are decided.
 template <int WH>
 __global__ void __launch_bounds__(kFilterThreads)
-dominance_kernel(FilterWork fw, int32_t n_valid) {
+dominance_kernel(FilterWork fw) {
     extern __shared__ __align__(16) uint32_t dyn_sh[];
     uint32_t* tile = dyn_sh;                                         // kTile x 2WH code words
     int32_t* tile_row = reinterpret_cast<int32_t*>(dyn_sh + kTile * 2 * WH);
+    __shared__ int32_t smax;
     const int Wh = fw.Wh;
     const int W2 = 2 * Wh;
-    const int32_t pos = blockIdx.x * kFilterThreads + threadIdx.x;
-    const bool active0 = pos < n_valid;
-    int32_t row = -1, limit = 0;
-    uint32_t P[WH], N[WH];
-    if (active0) {
-        row = fw.order[pos];
-        limit = fw.level_start[fw.l1[row]];  // rows with strictly smaller L1
+    const int32_t n_valid = fw.level_start[fw.Lmax + 1];
+    const int32_t nblk = (n_valid + kFilterThreads - 1) / kFilterThreads;
+    for (int32_t pb = blockIdx.x; pb < nblk; pb += gridDim.x) {
+        const int32_t pos = pb * kFilterThreads + threadIdx.x;
+        const bool active0 = pos < n_valid;
+        int32_t row = -1, limit = 0;
+        uint32_t P[WH], N[WH];
+        if (active0) {
+            row = fw.order[pos];
+            limit = fw.level_start[fw.l1[row]];  // rows with strictly smaller L1
 #pragma unroll
-        for (int w = 0; w < WH; ++w) {
-            P[w] = w < Wh ? fw.codes[(size_t)row * W2 + w] : 0u;
-            N[w] = w < Wh ? fw.codes[(size_t)row * W2 + Wh + w] : 0u;
-        }
-    }
-    bool done = !active0 || limit == 0;
-    int32_t wit = -1;
-    // block-wide scan limit
-    __shared__ int32_t smax;
-    if (threadIdx.x == 0) smax = 0;
-    __syncthreads();
-    if (active0) atomicMax(&smax, limit);
-    __syncthreads();
-    const int32_t maxlim = smax;
-    for (int32_t t0 = 0; t0 < maxlim; t0 += kTile) {
-        if (!__syncthreads_or(!done)) break;
-        for (int i = threadIdx.x; i < kTile; i += kFilterThreads) {
-            const int32_t q = t0 + i;
-            const int32_t hr = q < maxlim ? fw.order[q] : -1;
-            tile_row[i] = hr;
-            for (int w = 0; w < 2 * WH; ++w) {
-                const int half = w >= WH, ww = half ? w - WH : w;   // smem: P words [0,WH), N words [WH,2WH)
-                tile[i * 2 * WH + w] = (hr >= 0 && ww < Wh) ? fw.codes[(size_t)hr * W2 + half * Wh + ww] : 0u;
+            for (int w = 0; w < WH; ++w) {
+                P[w] = w < Wh ? fw.codes[(size_t)row * W2 + w] : 0u;
+                N[w] = w < Wh ? fw.codes[(size_t)row * W2 + Wh + w] : 0u;
             }
         }
+        bool done = !active0 || limit == 0;
+        int32_t wit = -1;
         __syncthreads();
-        if (!done) {
-            const int lim = min(kTile, limit - t0);
-            for (int i = 0; i < lim; ++i) {
-                const uint32_t* hc = &tile[i * 2 * WH];
-                uint32_t pos_v = 0, neg_v = 0;
-#pragma unroll
-                for (int w = 0; w < WH; ++w) {
-                    const uint32_t hp = hc[w], hn = hc[WH + w];
-                    pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
-                    neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
-                }
-                if (pos_v == 0u || neg_v == 0u) {
-                    done = true;
-                    wit = tile_row[i];
-                    break;
+        if (threadIdx.x == 0) smax = 0;
+        __syncthreads();
+        if (active0) atomicMax(&smax, limit);
+        __syncthreads();
+        const int32_t maxlim = smax;
+        for (int32_t t0 = 0; t0 < maxlim; t0 += kTile) {
+            if (!__syncthreads_or(!done)) break;
+            for (int i = threadIdx.x; i < kTile; i += kFilterThreads) {
+                const int32_t q = t0 + i;
+                const int32_t hr = q < maxlim ? fw.order[q] : -1;
+                tile_row[i] = hr;
+                for (int w = 0; w < 2 * WH; ++w) {
+                    const int half = w >= WH, ww = half ? w - WH : w;   // smem: P words [0,WH), N words [WH,2WH)
+                    tile[i * 2 * WH + w] = (hr >= 0 && ww < Wh) ? fw.codes[(size_t)hr * W2 + half * Wh + ww] : 0u;
                 }
             }
-            if (t0 + kTile >= limit) done = true;
+            __syncthreads();
+            if (!done) {
+                const int lim = min(kTile, limit - t0);
+                for (int i = 0; i < lim; ++i) {
+                    const uint32_t* hc = &tile[i * 2 * WH];
+                    uint32_t pos_v = 0, neg_v = 0;
+#pragma unroll
+                    for (int w = 0; w < WH; ++w) {
+                        const uint32_t hp = hc[w], hn = hc[WH + w];
+                        pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
+                        neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
+                    }
+                    if (pos_v == 0u || neg_v == 0u) {
+                        done = true;
+                        wit = tile_row[i];
+                        break;
+                    }
+                }
+                if (t0 + kTile >= limit) done = true;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
-    if (active0) {
-        fw.keep[row] = (wit < 0) ? 1 : 0;
-        fw.witness[row] = wit;
+        if (active0) {
+            fw.keep[row] = (wit < 0) ? 1 : 0;
+            fw.witness[row] = wit;
+        }
     }
 }
 
-__global__ void keep_all_kernel(const uint8_t* valid, int64_t count, uint8_t* keep, int32_t* witness) {
+__global__ void keep_valid_kernel(const uint8_t* valid, const unsigned long long* dcount, int64_t cap, uint8_t* keep,
+                                  int32_t* witness) {
+    const int64_t count = dev_count(dcount, cap);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
         keep[r] = valid[r];
         witness[r] = -1;
     }
 }
 
-__global__ void compact_kernel(const int8_t* __restrict__ rows, const uint8_t* sel, int64_t count, int n_pad,
-                               int8_t* out, unsigned long long* n_out) {
+__global__ void clear_keep_kernel(const unsigned long long* dcount, int64_t cap, uint8_t* keep) {
+    const int64_t count = dev_count(dcount, cap);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x)
+        keep[r] = 0;
+}
+
+__global__ void compact_kernel(const int8_t* __restrict__ rows, const uint8_t* sel, const unsigned long long* dcount,
+                               int64_t cap, int n_pad, int8_t* out, unsigned long long* n_out) {
     const int nw = n_pad / 16;
+    const int64_t count = dev_count(dcount, cap);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
         if (!sel[r]) continue;
         const unsigned long long o = atomicAdd(n_out, 1ULL);
@@ -373,68 +406,60 @@ __global__ void signed_union_kernel(const int8_t* __restrict__ rows, int64_t k, 
     }
 }
 
-inline unsigned grid_for(int64_t work, int threads = 256) {
+inline unsigned grid_for(int64_t work, int threads = 256, int64_t max_blocks = 148 * 16) {
     int64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
-    if (b > 148 * 32) b = 148 * 32;
+    if (b > max_blocks) b = max_blocks;
     return (unsigned)b;
 }
 
 }  // namespace
 
-cudaError_t launch_dedupe(const int8_t* rows, int64_t count, int row_stride, int n_pad, const HashSet& hs,
-                          cudaStream_t s) {
-    if (count <= 0) return cudaSuccess;
-    dedupe_kernel<<<grid_for(count), 256, 0, s>>>(rows, count, row_stride, n_pad, hs);
+cudaError_t launch_dedupe(const int8_t* rows, const unsigned long long* dcount, int64_t cap, int row_stride,
+                          int n_pad, const HashSet& hs, cudaStream_t s) {
+    if (cap <= 0) return cudaSuccess;
+    dedupe_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(rows, dcount, cap, row_stride, n_pad, hs);
     return cudaGetLastError();
 }
 
-cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& cp, uint8_t* flags,
-                         unsigned long long* n_bad, cudaStream_t s) {
-    if (count <= 0) return cudaSuccess;
-    const size_t smem = (size_t)(((cp.m + 1 + 2 * cp.nnz + cp.n) + 3) & ~3) * 4 + (size_t)kCheckThreads * cp.n_pad;
+cudaError_t launch_check_codes(const int8_t* rows, const unsigned long long* dcount, int64_t cap, const CheckParams& cp,
+                               FilterWork& fw, int encode, uint8_t* flags, unsigned long long* n_bad, cudaStream_t s) {
+    if (cap <= 0) return cudaSuccess;
+    const size_t smem = (size_t)(((cp.m + 1 + 2 * cp.nnz + 2 * cp.n + 2 * fw.Wh) + 3) & ~3) * 4 +
+                        (size_t)kCheckThreads * (cp.n_pad + 16);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    cudaError_t e = cudaFuncSetAttribute(check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(check_codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    int64_t blocks = (count + kCheckThreads - 1) / kCheckThreads;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    check_kernel<<<(unsigned)blocks, kCheckThreads, smem, s>>>(rows, count, cp, flags, n_bad);
+    check_codes_kernel<<<grid_for(cap, kCheckThreads, 148 * 8), kCheckThreads, smem, s>>>(rows, dcount, cap, cp, fw,
+                                                                                          flags, n_bad, encode);
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t count, FilterWork& fw,
+cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const uint8_t* valid, FilterWork& fw,
                           int filter_minimal, cudaStream_t s, int* launches) {
-    if (count <= 0) return cudaSuccess;
+    if (cap <= 0) return cudaSuccess;
     if (!filter_minimal) {
-        keep_all_kernel<<<grid_for(count), 256, 0, s>>>(valid, count, fw.keep, fw.witness);
+        keep_valid_kernel<<<grid_for(cap), 256, 0, s>>>(valid, dcount, cap, fw.keep, fw.witness);
         *launches += 1;
         return cudaGetLastError();
     }
     cudaError_t e;
-    codes_kernel<<<grid_for(count * 2 * fw.Wh), 256, 0, s>>>(rows, valid, count, fw);
-    if ((e = cudaMemsetAsync(fw.hist, 0, sizeof(int32_t) * (fw.Lmax + 2), s)) != cudaSuccess) return e;
     const int nb = fw.Lmax + 1;
-    hist_kernel<<<std::min<unsigned>(grid_for(count), 148 * 4), 256, nb * 4, s>>>(fw.l1, count, fw.hist, nb);
+    if ((e = cudaMemsetAsync(fw.hist, 0, sizeof(int32_t) * (fw.Lmax + 2), s)) != cudaSuccess) return e;
+    hist_kernel<<<grid_for(cap, 256, 148 * 4), 256, nb * 4, s>>>(fw.l1, dcount, cap, fw.hist, nb);
     scan_kernel<<<1, 32, 0, s>>>(fw.hist, nb, fw.level_start, fw.cursor);
-    scatter_kernel<<<std::min<unsigned>(grid_for((count + 7) / 8), 148 * 4), 256, 2 * nb * 4, s>>>(
-        fw.l1, count, fw.cursor, fw.order, nb);
+    scatter_kernel<<<grid_for((cap + 7) / 8, 256, 148 * 4), 256, 2 * nb * 4, s>>>(fw.l1, dcount, cap, fw.cursor,
+                                                                                  fw.order, nb);
+    clear_keep_kernel<<<grid_for(cap), 256, 0, s>>>(dcount, cap, fw.keep);
     *launches += 4;
-    // number of valid rows = level_start[Lmax + 1]; read on host to size the grid
-    int32_t n_valid = 0;
-    if ((e = cudaMemcpyAsync(&n_valid, fw.level_start + fw.Lmax + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s)) !=
-        cudaSuccess)
-        return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(fw.keep, 0, count, s)) != cudaSuccess) return e;
-    if (n_valid == 0) return cudaSuccess;
-    const unsigned blocks = (unsigned)((n_valid + kFilterThreads - 1) / kFilterThreads);
+    const unsigned blocks = grid_for(cap, kFilterThreads, 148 * 4);
 #define MAPLE_DOM(WHV)                                                                                       \
     if (fw.Wh <= WHV) {                                                                                      \
         const size_t sm = (size_t)kTile * (2 * WHV + 1) * 4;                                                 \
         if ((e = cudaFuncSetAttribute(dominance_kernel<WHV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                       (int)sm)) != cudaSuccess)                                              \
             return e;                                                                                        \
-        dominance_kernel<WHV><<<blocks, kFilterThreads, sm, s>>>(fw, n_valid);                              \
+        dominance_kernel<WHV><<<blocks, kFilterThreads, sm, s>>>(fw);                                        \
     } else
     MAPLE_DOM(1) MAPLE_DOM(2) MAPLE_DOM(4) MAPLE_DOM(8) MAPLE_DOM(16) MAPLE_DOM(32) return cudaErrorInvalidValue;
 #undef MAPLE_DOM
@@ -448,10 +473,10 @@ cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, int64_t count, int n_pad, int8_t* out,
-                           unsigned long long* n_out, cudaStream_t s) {
-    if (count <= 0) return cudaSuccess;
-    compact_kernel<<<grid_for(count), 256, 0, s>>>(rows, sel, count, n_pad, out, n_out);
+cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, const unsigned long long* dcount, int64_t cap,
+                           int n_pad, int8_t* out, unsigned long long* n_out, cudaStream_t s) {
+    if (cap <= 0) return cudaSuccess;
+    compact_kernel<<<grid_for(cap), 256, 0, s>>>(rows, sel, dcount, cap, n_pad, out, n_out);
     return cudaGetLastError();
 }
 

@@ -46,11 +46,12 @@ struct HashSet {
     int64_t pool_cap;
     unsigned long long* pool_count;
     int* overflow;
+    unsigned long long* max_count;  // running max of the input counts (detects candidate-buffer overflow)
 };
 
-// Insert rows (stride n_pad) into the set; new unique rows are appended to the pool.
-cudaError_t launch_dedupe(const int8_t* rows, int64_t count, int row_stride, int n_pad, const HashSet& hs,
-                          cudaStream_t s);
+// Insert min(*dcount, cap) rows (stride row_stride) into the set; new unique rows are appended to the pool.
+cudaError_t launch_dedupe(const int8_t* rows, const unsigned long long* dcount, int64_t cap, int row_stride,
+                          int n_pad, const HashSet& hs, cudaStream_t s);
 
 struct CheckParams {
     int m, n, n_pad;
@@ -60,10 +61,6 @@ struct CheckParams {
     int nnz;
     const int32_t* box;           // u - l
 };
-// flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= box (conditions C1-C3).
-cudaError_t launch_check(const int8_t* rows, int64_t count, const CheckParams& cp, uint8_t* flags,
-                         unsigned long long* n_bad, cudaStream_t s);
-
 struct FilterWork {
     int n, n_pad;
     int Lh, Wh;                   // thermometer bits per half, 32-bit words per half
@@ -80,12 +77,16 @@ struct FilterWork {
     int32_t* witness;             // count
     int Lmax;
 };
-cudaError_t launch_filter(const int8_t* rows, const uint8_t* valid, int64_t count, FilterWork& fw,
+// flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= u - l (conditions C1-C3), for the first
+// min(*dcount, cap) rows; with encode != 0 also the filter's thermometer codes and L1 norms.
+cudaError_t launch_check_codes(const int8_t* rows, const unsigned long long* dcount, int64_t cap, const CheckParams& cp,
+                               FilterWork& fw, int encode, uint8_t* flags, unsigned long long* n_bad, cudaStream_t s);
+// keep[r] (and witness[r]) for the ⊑ filter, or keep = valid when filter_minimal == 0
+cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const uint8_t* valid, FilterWork& fw,
                           int filter_minimal, cudaStream_t s, int* launches);
-
 // Gather rows with sel[r] != 0 into out (stride n_pad) in an arbitrary order; count to *n_out (device).
-cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, int64_t count, int n_pad, int8_t* out,
-                           unsigned long long* n_out, cudaStream_t s);
+cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, const unsigned long long* dcount, int64_t cap,
+                           int n_pad, int8_t* out, unsigned long long* n_out, cudaStream_t s);
 // Lexicographic sort of k rows (stride n_pad, n bytes compared as signed int8). keys/idx scratch:
 // keys: k * n_pad/4 uint32, idx0/idx1: k int32. Result written to out rows.
 cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uint32_t* keys, int32_t* idx0,
