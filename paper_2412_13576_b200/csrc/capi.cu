@@ -318,7 +318,7 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
 }
 
 cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
-    const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2048.0;
+    const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
     const bool tc = ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && tc_ok);
     ctx->launches++;
     if (tc) return launch_descent_tc(p, ctx->stream);
@@ -331,7 +331,7 @@ int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t 
     if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
     if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
     if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
-    if (ctx->descent_kernel == 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2048.0))
+    if (ctx->descent_kernel == 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
         FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
     return MAPLE_OK;
 }

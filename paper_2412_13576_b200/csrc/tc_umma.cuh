@@ -63,23 +63,25 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 
 __device__ __forceinline__ bool mbar_try(uint32_t a, uint32_t parity) {
     uint32_t ok;
+    // try_wait with a suspend-time hint: the thread sleeps in hardware until the phase completes (or the
+    // hint expires) instead of re-issuing the probe
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}\n"
         : "=r"(ok)
-        : "r"(a), "r"(parity)
+        : "r"(a), "r"(parity), "r"(0x989680u)
         : "memory");
     return ok != 0;
 }
 
 // Wait for the mbarrier phase with the given parity. A watchdog traps (kernel error, no GPU hang) if the
-// phase never completes (~several seconds of try_wait).
+// phase never completes.
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     const uint32_t a = smem_u32(mbar);
     uint32_t spins = 0;
     while (!mbar_try(a, parity)) {
-        if (++spins > (1u << 26)) asm volatile("trap;");
+        if (++spins > (1u << 22)) asm volatile("trap;");
     }
 }
 

@@ -1,0 +1,117 @@
+"""Parity at BASELINE.json's full sizes in the launch configuration bench.py times (configs[1] = C2a,
+65,536 starts, T=200), on sampled outputs the oracle can compute, plus properties that hold at any size;
+and the larger configs (C3 n=300, C5 n=1000) at sizes the oracle finishes in seconds."""
+import numpy as np
+import pytest
+
+from oracle import extraction as OX
+from oracle import graver as OG
+from oracle import postprocess as OP
+
+pytestmark = pytest.mark.gpu
+
+
+def _set(rows):
+    return {tuple(int(v) for v in r) for r in np.asarray(rows).tolist()}
+
+
+def _closed_semi(k, s):
+    out = set()
+    for r in range(k):
+        for i in range(s):
+            for j in range(i + 1, s):
+                v = [0] * (k * s)
+                v[r * s + i], v[r * s + j] = 1, -1
+                out.add(tuple(v))
+    return out
+
+
+def test_c2a_full_bench_configuration(gpu_lib):
+    """Full run (the bench's extract call): every output row is a Graver element of the closed form, the set
+    is an antichain, canonical and sorted, and it is the complete Graver basis (225 = 5 C(10,2))."""
+    from synth import c2a
+    inst = c2a()
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    ds = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
+    rows = ds.rows()
+    S = _set(rows)
+    assert np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
+    assert [tuple(r) for r in rows.tolist()] == sorted(S)                  # lexicographic output order
+    assert all(OG.canonical(g) == g for g in S)                            # first nonzero > 0
+    assert OP.is_antichain(S)
+    assert S == _closed_semi(5, 10)
+    # determinism across runs
+    np.testing.assert_array_equal(ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows(), rows)
+
+
+def test_c2a_full_sampled_starts_vs_oracle(gpu_lib):
+    """Sampled outputs at the full launch: starts [0, 512) of the 65,536-start run (same global indices,
+    so the same trajectories as inside the full run): final iterates gate G2, and their harvest sets G3."""
+    from synth import c2a
+    inst = c2a()
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    S_ = 512
+    Z, _ = ctx.debug_descent(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed)
+    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(S_))
+    Z64 = OX.descend(z0, ctx.B, inst.steps, inst.lr)
+    Z32 = OX.descend(z0.astype(np.float32), ctx.B, inst.steps, inst.lr, dtype=np.float32)
+
+    def pf(A, R):
+        return float(np.mean(np.all(np.abs(A.astype(np.float64) - R) / np.maximum(1, np.abs(R)) <= 1e-4, axis=1)))
+    assert pf(Z, Z64) >= pf(Z32, Z64) - 0.02
+    part = _set(ctx.extract_range(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed).rows())
+    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
+                              starts=np.arange(S_))
+    ora = OP.minimal_filter(pool)
+    j = len(part & ora) / max(1, len(part | ora))
+    assert j >= 0.99
+    # the sampled range's minimal set is a subset of the full run's support (union over partitions)
+    full = _set(ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows())
+    assert all(any(OG.conforms(h, g) or OG.conforms(h, tuple(-x for x in g)) for h in full) for g in part)
+
+
+def test_c2a_full_postprocess_witnesses(gpu_lib):
+    """G1 at full size with the unfiltered pool (757k rows): the GPU's pool equals the oracle dedupe of the
+    GPU candidate multiset, and the ⊑-minimal output is verified in O(K M): no output row is dominated by
+    any pool row, and every pool row is dominated by (or equal to) an output row."""
+    from synth import c2a
+    inst = c2a()
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    ctx.set_params(filter_minimal=False)
+    pool = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows()
+    ctx.set_params(filter_minimal=True)
+    mins = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows()
+    assert np.all(OP.check_rows(inst.A, inst.l, inst.u, pool))
+    P = pool.astype(np.int8)
+    aP = np.abs(P)
+    sP = np.sign(P)
+    for g in mins.astype(np.int8):
+        ag, sg = np.abs(g), np.sign(g)
+        le = np.all(aP <= ag, axis=1)
+        dom = le & (np.all(sP * sg >= 0, axis=1) | np.all(sP * sg <= 0, axis=1))
+        assert dom.sum() == 1                     # only itself
+    covered = np.zeros(len(P), dtype=bool)
+    for h in mins.astype(np.int8):
+        ah, sh = np.abs(h), np.sign(h)
+        covered |= np.all(ah[None, :] <= aP, axis=1) & (np.all(sP * sh >= 0, axis=1) | np.all(sP * sh <= 0, axis=1))
+    assert covered.all()
+
+
+@pytest.mark.parametrize("name,N,T", [("C3", 128, 40), ("C5", 64, 30)])
+def test_large_configs_small_sizes(gpu_lib, name, N, T):
+    """C3 (n=300, m=20) and C5 (n=1000, m=100) through the general path at oracle-sized N: bit-exact
+    post-processing of the GPU candidates (G1) and iterate agreement at small T (G2)."""
+    from synth import config
+    inst = config(name)
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    assert np.all(inst.A @ ctx.B == 0)
+    Z, _ = ctx.debug_descent(N, 0, N, 3, inst.lr, inst.seed)
+    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
+    Zo = OX.descend(z0, ctx.B, 3, inst.lr)
+    assert float(np.mean(np.all(np.abs(Z - Zo) / np.maximum(1, np.abs(Zo)) <= 1e-4, axis=1))) >= 0.99
+    ctx.set_debug(True)
+    ds = ctx.extract(N, T, inst.lr, inst.seed)
+    cand = ctx.candidates()
+    ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, cand)
+    assert nbad == 0
+    assert [tuple(r) for r in ds.rows().tolist()] == ref
