@@ -63,6 +63,8 @@ struct maple_ctx {
     std::vector<double> Bp;       // d x n
     // device constants
     DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, th_off, th_c0, th_c1;
+    DevBuf sb_rptr, sb_rcol, sb_rval, sb_cptr, sb_crow, sb_cval, sb_lrp, sb_lr, sb_lcp, sb_lc;
+    SparseB sb{};
     int nnz = 0, Lh = 0, Wh = 0;
     double rbound = 0;            // max_j sum_i |B+_ji| (u_i - l_i): bound on |round(z)| of any in-box g
     // params (Eq. 3 / Adam)
@@ -310,6 +312,7 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.B_nd = ctx->B_nd.as<float>();
     p.B_dn = ctx->B_dn.as<float>();
     p.B8_nd = ctx->B8.as<int8_t>();
+    p.sb = ctx->sb;
     p.Bp = ctx->dBp.as<double>();
     p.lo = ctx->dl.as<int32_t>();
     p.hi = ctx->du.as<int32_t>();
@@ -446,6 +449,80 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->B_dn, bdn));
     CU(upload(ctx->B8, b8));
     CU(upload(ctx->dBp, ctx->Bp));
+    {   // sparse B (CSR, CSC) + load-balanced lane lists for the SIMT path
+        std::vector<int32_t> rptr(n + 1, 0), cptr(d + 1, 0);
+        std::vector<int16_t> rcol, crow;
+        std::vector<float> rval, cval;
+        for (int i = 0; i < n; ++i) {
+            for (int j = 0; j < d; ++j)
+                if (ctx->B[(size_t)i * d + j]) {
+                    rcol.push_back((int16_t)j);
+                    rval.push_back((float)ctx->B[(size_t)i * d + j]);
+                }
+            rptr[i + 1] = (int32_t)rcol.size();
+        }
+        for (int j = 0; j < d; ++j) {
+            for (int i = 0; i < n; ++i)
+                if (ctx->B[(size_t)i * d + j]) {
+                    crow.push_back((int16_t)i);
+                    cval.push_back((float)ctx->B[(size_t)i * d + j]);
+                }
+            cptr[j + 1] = (int32_t)crow.size();
+        }
+        auto lanes = [](const std::vector<int32_t>& ptr, int cnt, std::vector<int32_t>& lp, std::vector<int32_t>& lst) {
+            std::vector<int> idx(cnt);
+            for (int i = 0; i < cnt; ++i) idx[i] = i;
+            std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+                return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b];
+            });
+            std::vector<std::vector<int32_t>> per(32);
+            for (int p = 0; p < cnt; ++p) {
+                const int blk = p / 32, off = p % 32;
+                per[(blk & 1) ? 31 - off : off].push_back(idx[p]);
+            }
+            lp.assign(33, 0);
+            lst.clear();
+            int mx = 0;
+            for (int L = 0; L < 32; ++L) {
+                std::sort(per[L].begin(), per[L].end());
+                lst.insert(lst.end(), per[L].begin(), per[L].end());
+                lp[L + 1] = (int32_t)lst.size();
+                mx = std::max(mx, (int)per[L].size());
+            }
+            return mx;
+        };
+        std::vector<int32_t> lrp, lr, lcp, lc;
+        lanes(rptr, n, lrp, lr);
+        const int mxc = lanes(cptr, d, lcp, lc);
+        const int nnzb = (int)rcol.size();
+        CU(upload(ctx->sb_rptr, rptr));
+        CU(upload(ctx->sb_rcol, rcol));
+        CU(upload(ctx->sb_rval, rval));
+        CU(upload(ctx->sb_cptr, cptr));
+        CU(upload(ctx->sb_crow, crow));
+        CU(upload(ctx->sb_cval, cval));
+        CU(upload(ctx->sb_lrp, lrp));
+        CU(upload(ctx->sb_lr, lr));
+        CU(upload(ctx->sb_lcp, lcp));
+        CU(upload(ctx->sb_lc, lc));
+        SparseB& sb = ctx->sb;
+        sb.nnz = nnzb;
+        sb.max_lane_cols = mxc;
+        sb.smem_bytes = (((size_t)(n + 1 + d + 1) * 4 + (size_t)nnzb * 12) + 15) & ~size_t(15);
+        const size_t per_warp = std::max<size_t>((size_t)(2 * d + n) * 4, (size_t)n * 8);
+        sb.in_smem = (sb.smem_bytes + ((per_warp + 15) & ~size_t(15)) * 8) <= 100 * 1024 ? 1 : 0;
+        sb.row_ptr = ctx->sb_rptr.as<int32_t>();
+        sb.row_col = ctx->sb_rcol.as<int16_t>();
+        sb.row_val = ctx->sb_rval.as<float>();
+        sb.col_ptr = ctx->sb_cptr.as<int32_t>();
+        sb.col_row = ctx->sb_crow.as<int16_t>();
+        sb.col_val = ctx->sb_cval.as<float>();
+        sb.lane_rows_ptr = ctx->sb_lrp.as<int32_t>();
+        sb.lane_rows = ctx->sb_lr.as<int32_t>();
+        sb.lane_cols_ptr = ctx->sb_lcp.as<int32_t>();
+        sb.lane_cols = ctx->sb_lc.as<int32_t>();
+        if (mxc > 32) return MAPLE_ERR_RANGE;  // d > 1024
+    }
     CU(upload(ctx->th_off, toff));
     CU(upload(ctx->th_c0, wc0));
     CU(upload(ctx->th_c1, wc1));
@@ -481,7 +558,9 @@ void maple_destroy(maple_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     g_alloc_stream = ctx->stream;
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
-                      &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1, &ctx->step_tab, &ctx->cand,
+                      &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
+                      &ctx->sb_rptr, &ctx->sb_rcol, &ctx->sb_rval, &ctx->sb_cptr, &ctx->sb_crow, &ctx->sb_cval,
+                      &ctx->sb_lrp, &ctx->sb_lr, &ctx->sb_lcp, &ctx->sb_lc, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,

@@ -5,6 +5,23 @@
 
 namespace maple {
 
+// Sparse B for the SIMT path: CSR (rows i, for B z and B r), CSC (columns j, for B^T s) and load-balanced
+// per-lane row / column lists (snake order by nonzero count). Column lists bound the per-lane Adam state.
+struct SparseB {
+    int nnz, in_smem, max_lane_cols;
+    size_t smem_bytes;            // bytes of the shared-memory copy (CSR + CSC)
+    const int32_t* row_ptr;       // n + 1
+    const int16_t* row_col;       // nnz
+    const float* row_val;         // nnz
+    const int32_t* col_ptr;       // d + 1
+    const int16_t* col_row;       // nnz
+    const float* col_val;         // nnz
+    const int32_t* lane_rows_ptr; // 33
+    const int32_t* lane_rows;     // n
+    const int32_t* lane_cols_ptr; // 33
+    const int32_t* lane_cols;     // d
+};
+
 struct DescentParams {
     int n, d, n_pad, T;
     float lam1, lam2, beta1, beta2, eps;
@@ -16,6 +33,7 @@ struct DescentParams {
     const float* B_nd;            // B, n x d row-major (fp32, exact small integers)
     const float* B_dn;            // B^T, d x n row-major
     const int8_t* B8_nd;          // B as int8, n x d
+    SparseB sb;                   // sparse B (SIMT path)
     const double* Bp;             // B+, d x n row-major
     const int32_t* lo;            // l (n)
     const int32_t* hi;            // u (n)
