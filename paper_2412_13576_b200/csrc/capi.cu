@@ -98,6 +98,7 @@ struct maple_dirset {
     int16_t* D_col = nullptr;
     int8_t* D_val = nullptr;
     int D_nzmax = 0;
+    cudaEvent_t ready = nullptr;  // recorded after the last device write to this set
 };
 
 // counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
@@ -222,7 +223,7 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     ds->size = M;
     ds->pool_size = (int64_t)h[C_POOL] - (int64_t)h[C_BAD];
     ds->n_bad = (int64_t)h[C_BAD];
-    cudaError_t e = cudaMalloc(&ds->rows, std::max<int64_t>(M, 1) * np);
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ds->rows), std::max<int64_t>(M, 1) * np, s);
     if (e != cudaSuccess) {
         delete ds;
         CU(e);
@@ -235,6 +236,7 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
                        ctx->sidx1.as<int32_t>(), ds->rows, s, &nl));
     ctx->launches += nl;
     CU(cudaEventRecord(ctx->ev[5], s));
+    if (cudaEventCreateWithFlags(&ds->ready, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(ds->ready, s);
     ctx->timings_pending = true;
     *out = ds;
     return MAPLE_OK;
@@ -784,11 +786,16 @@ int maple_dirset_copy_device(const maple_dirset* ds, int8_t* dst) {
 
 void maple_dirset_free(maple_dirset* ds) {
     if (!ds) return;
-    if (ds->rows) cudaFree(ds->rows);
-    if (ds->D) cudaFree(ds->D);
-    if (ds->D_nnz) cudaFree(ds->D_nnz);
-    if (ds->D_col) cudaFree(ds->D_col);
-    if (ds->D_val) cudaFree(ds->D_val);
+    // wait for the producing work, then stream-ordered frees back to the pool
+    if (ds->ready) {
+        cudaEventSynchronize(ds->ready);
+        cudaEventDestroy(ds->ready);
+    }
+    if (ds->rows) cudaFreeAsync(ds->rows, 0);
+    if (ds->D) cudaFreeAsync(ds->D, 0);
+    if (ds->D_nnz) cudaFreeAsync(ds->D_nnz, 0);
+    if (ds->D_col) cudaFreeAsync(ds->D_col, 0);
+    if (ds->D_val) cudaFreeAsync(ds->D_val, 0);
     delete ds;
 }
 
@@ -858,7 +865,7 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
         CU(un.ensure((size_t)2 * K * np));
         CU(launch_signed_union(ds->rows, K, np, un.as<int8_t>(), s));
         ctx->launches++;
-        CU(cudaMalloc(&dsm->D, (size_t)2 * K * np));
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D), (size_t)2 * K * np, s));
         CU(ctx->sortkeys.ensure((size_t)2 * K * np));
         CU(ctx->sidx0.ensure((size_t)2 * K * 4));
         CU(ctx->sidx1.ensure((size_t)2 * K * 4));
@@ -868,7 +875,7 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
         ctx->launches += nl;
         CU(cudaStreamSynchronize(s));
         un.release();
-        CU(cudaMalloc(&dsm->D_nnz, (size_t)2 * K * sizeof(int32_t)));
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_nnz), (size_t)2 * K * sizeof(int32_t), s));
         DevBuf nzd;
         CU(nzd.ensure(sizeof(int)));
         CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, dsm->D_nnz, nzd.as<int>(), &dsm->D_col, &dsm->D_val,

@@ -82,12 +82,13 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
 }
 
 __global__ void __launch_bounds__(kAugThreads)
-augment_kernel(AugmentParams p) {
+augment_kernel(AugmentParams p, int staged) {
     __shared__ int32_t x[kMaxN];
     __shared__ double grad[kMaxN];
     __shared__ Cand wbest[kAugThreads / 32];
     __shared__ Cand best_sh;
     __shared__ double f2_sh;
+    extern __shared__ __align__(16) unsigned char dsm[];   // staged D (ELL) + q_g when it fits
     const int inc = blockIdx.x;  // incumbent index over all instances
     const int inst = inc / p.k0;
     const int n = p.n;
@@ -95,6 +96,25 @@ augment_kernel(AugmentParams p) {
     const double* c = p.c + (size_t)inst * n;
     const double* qg = p.qg + (size_t)inst * 2 * p.n_dir;
     int32_t* xg = p.X + (size_t)inc * n;
+    if (staged) {
+        const int nD2 = 2 * p.n_dir, nz = p.nzmax;
+        double* s_qg = reinterpret_cast<double*>(dsm);
+        int32_t* s_nnz = reinterpret_cast<int32_t*>(s_qg + nD2);
+        int16_t* s_col = reinterpret_cast<int16_t*>(s_nnz + nD2);
+        int8_t* s_val = reinterpret_cast<int8_t*>(s_col + (size_t)nD2 * nz);
+        for (int e = threadIdx.x; e < nD2; e += blockDim.x) {
+            s_qg[e] = qg[e];
+            s_nnz[e] = p.nnz[e];
+        }
+        for (int e = threadIdx.x; e < nD2 * nz; e += blockDim.x) {
+            s_col[e] = p.col[e];
+            s_val[e] = p.val[e];
+        }
+        qg = s_qg;
+        p.nnz = s_nnz;
+        p.col = s_col;
+        p.val = s_val;
+    }
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xg[i];
     __syncthreads();
     // ∇ = Q x + c ; 2 f(x) = x^T Q x + 2 c^T x + 2 c0
@@ -238,8 +258,9 @@ cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int
     if ((e = cudaMemcpyAsync(nzmax_host, nzmax_dev, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
     const int nz = std::max(*nzmax_host, 1);
-    if ((e = cudaMalloc(col, (size_t)nD * nz * sizeof(int16_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(val, (size_t)nD * nz)) != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(col), (size_t)nD * nz * sizeof(int16_t), s)) != cudaSuccess)
+        return e;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(val), (size_t)nD * nz, s)) != cudaSuccess) return e;
     ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, nz, *col, *val);
     *nzmax_host = nz;
     return cudaGetLastError();
@@ -270,7 +291,14 @@ cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s) {
     if (p.n > kMaxN) return cudaErrorInvalidValue;
     const int64_t blocks = (int64_t)p.n_inst * p.k0;
     if (blocks <= 0) return cudaSuccess;
-    augment_kernel<<<(unsigned)blocks, kAugThreads, 0, s>>>(p);
+    const size_t nD2 = (size_t)2 * p.n_dir;
+    const size_t smem = nD2 * 8 + nD2 * 4 + nD2 * p.nzmax * 3 + 16;
+    const int staged = smem <= 96 * 1024;
+    if (staged && smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    augment_kernel<<<(unsigned)blocks, kAugThreads, staged ? smem : 0, s>>>(p, staged);
     return cudaGetLastError();
 }
 
