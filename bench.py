@@ -35,6 +35,21 @@ N_STARTS, T_STEPS, LR, SEED = 65536, 200, 0.01, 2
 K_INCUMBENTS = 100
 
 
+def _set_workload(name, n_starts=0):
+    """Switch the module-level workload constants to another BASELINE config (secondary measurements)."""
+    global WORKLOAD, N_STARTS, T_STEPS, LR, SEED
+    from synth import config
+    inst = config(name)
+    WORKLOAD = name
+    N_STARTS = n_starts or inst.n_starts
+    T_STEPS, LR, SEED = inst.steps, inst.lr, inst.seed
+
+
+def _instance():
+    from synth import config
+    return config(WORKLOAD)
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -100,14 +115,14 @@ def run_reference(args):
     if rank != 0:
         return 0
     from oracle import augment as OA, extraction as OX, lattice as OL, postprocess as OP
-    from synth import c2a, feasible_points
+    from synth import feasible_points
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    inst = c2a()
-    S, KI = 256, 10
+    inst = _instance()
+    S, KI = (256, 10) if inst.n <= 64 else (16, 2)
     times, nset = [], 0
     for it in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -144,14 +159,14 @@ def run_reference(args):
 def cpu_baseline_sample():
     """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
     from oracle import augment as OA, extraction as OX, lattice as OL, postprocess as OP
-    from synth import c2a, feasible_points
+    from synth import feasible_points
     try:
         from threadpoolctl import threadpool_info
         cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
         cores = os.cpu_count()
-    inst = c2a()
-    S, KI = 1024, 20
+    inst = _instance()
+    S, KI = (1024, 20) if inst.n <= 64 else (32, 4)
     t0 = time.perf_counter()
     B = np.array(OL.lll_reduce(OL.kernel_basis(inst.A)), dtype=np.int64)
     pool, _ = OX.extract_pool(B, OL.pinv(B), inst.l, inst.u, N_STARTS, T_STEPS, LR, SEED, starts=np.arange(S))
@@ -178,7 +193,11 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--descent-kernel", type=int, default=0)
+    ap.add_argument("--workload", default="C2a", choices=["C1", "C2a", "C2b", "C3", "C5"],
+                    help="configs[1] (C2a) is the headline line; the others are secondary measurements")
+    ap.add_argument("--n-starts", type=int, default=0, help="override the workload's start count")
     args = ap.parse_args()
+    _set_workload(args.workload, args.n_starts)
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
@@ -197,10 +216,10 @@ def main():
         dist.barrier()
     from paper_2412_13576_b200 import maple
     from paper_2412_13576_b200 import distributed as D
-    from synth import c2a, feasible_points
+    from synth import feasible_points
 
     maple.load()
-    inst = c2a()
+    inst = _instance()
     X0 = feasible_points(inst, K_INCUMBENTS, seed=99)
     stream = torch.cuda.Stream()
     t_c0 = time.perf_counter()

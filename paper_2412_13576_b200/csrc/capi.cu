@@ -66,7 +66,8 @@ struct maple_ctx {
     DevBuf sb_rptr, sb_rcol, sb_rval, sb_cptr, sb_crow, sb_cval, sb_lrp, sb_lr, sb_lcp, sb_lc;
     SparseB sb{};
     int nnz = 0, Lh = 0, Wh = 0;
-    double rbound = 0;            // max_j sum_i |B+_ji| (u_i - l_i): bound on |round(z)| of any in-box g
+    double rbound = 0;
+    int binary = 0;               // every u_i - l_i == 1            // max_j sum_i |B+_ji| (u_i - l_i): bound on |round(z)| of any in-box g
     // params (Eq. 3 / Adam)
     double lam1 = 0.85, lam2 = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
     int filter_minimal = 1;
@@ -191,7 +192,7 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
                    ctx->nnz, ctx->dbox.as<int32_t>()};
     if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
-    FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
+    FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->binary, ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
                   ctx->th_c1.as<int32_t>(), ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
                   ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh};
@@ -428,6 +429,8 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     }
     ctx->Lh = lh;
     ctx->Wh = (ctx->Lh + 31) / 32;
+    ctx->binary = 1;
+    for (int i = 0; i < n; ++i) ctx->binary &= (ctx->box[i] == 1);
     std::vector<int32_t> wc0(std::max(ctx->Wh, 1), 0), wc1(std::max(ctx->Wh, 1), -1);
     for (int w = 0; w < ctx->Wh; ++w) {
         int c0 = -1, c1 = -1;

@@ -65,7 +65,15 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned lo
             if (cur == 0ULL) {
                 cur = atomicCAS(&hs.keys[pos], 0ULL, key);
                 if (cur == 0ULL) {  // we own the slot: publish a new unique row
-                    const unsigned long long idx = atomicAdd(hs.pool_count, 1ULL);
+                    // opportunistic warp aggregation of the pool-index allocation (one atomic per group of
+                    // lanes that reach this point together instead of one per new row)
+                    const unsigned am = __activemask();
+                    const int lane = threadIdx.x & 31;
+                    const int leader = __ffs(am) - 1;
+                    unsigned long long base = 0;
+                    if (lane == leader) base = atomicAdd(hs.pool_count, (unsigned long long)__popc(am));
+                    base = __shfl_sync(am, base, leader);
+                    const unsigned long long idx = base + __popc(am & ((1u << lane) - 1u));
                     if ((int64_t)idx >= hs.pool_cap) {
                         atomicExch(hs.overflow, 1);
                         atomicExch(&hs.idx[pos], -2);
@@ -137,11 +145,21 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
         const int8_t* g = srow + threadIdx.x * stride;
         bool ok = true, nz = false;
         int l1 = 0;
-        for (int i = 0; i < cp.n; ++i) {
-            const int v = g[i];
-            nz |= (v != 0);
-            ok &= (abs(v) <= sbox[i]);
-            l1 += abs(v);
+        if (fw.binary) {  // every u_i - l_i == 1: |g_i| <= 1, bytewise on 16-byte words
+            const uint32_t* gw = reinterpret_cast<const uint32_t*>(g);
+            for (int w = 0; w < cp.n_pad / 4; ++w) {
+                const uint32_t a = __vabsss4(gw[w]);
+                ok &= (a & 0xFEFEFEFEu) == 0u;
+                nz |= a != 0u;
+                l1 += (int)__vsadu4(a, 0u);
+            }
+        } else {
+            for (int i = 0; i < cp.n; ++i) {
+                const int v = g[i];
+                nz |= (v != 0);
+                ok &= (abs(v) <= sbox[i]);
+                l1 += abs(v);
+            }
         }
         for (int a = 0; a < cp.m && ok; ++a) {
             long long acc = 0;
@@ -156,6 +174,24 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
             fw.l1[r] = ok ? l1 : -1;
             // thermometer code: coordinate i owns bits [off_i, off_i + u_i - l_i) of each half
             uint32_t* code = fw.codes + (size_t)r * W2;
+            if (fw.binary && ok) {  // bit i of P = [g_i > 0], of N = [g_i < 0] (off_i = i)
+                const uint32_t* gw = reinterpret_cast<const uint32_t*>(g);
+                for (int w = 0; w < fw.Wh; ++w) {
+                    uint32_t pw = 0, nw_ = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const int wi = 8 * w + q;
+                        const uint32_t x = wi < cp.n_pad / 4 ? gw[wi] : 0u;
+                        const uint32_t pos = __vcmpgts4(x, 0u) & 0x01010101u;    // byte > 0
+                        const uint32_t neg = (x >> 7) & 0x01010101u;              // byte < 0
+                        // gather bit 8k of each byte into bit k: (x * 0x01020408) >> 24 (no carries)
+                        pw |= (((pos * 0x01020408u) >> 24) & 0xFu) << (4 * q);
+                        nw_ |= (((neg * 0x01020408u) >> 24) & 0xFu) << (4 * q);
+                    }
+                    code[w] = pw;
+                    code[fw.Wh + w] = nw_;
+                }
+            } else
             for (int hf = 0; hf < 2; ++hf) {
                 for (int w = 0; w < fw.Wh; ++w) {
                     uint32_t word = 0;
@@ -388,6 +424,61 @@ __global__ void merge_pass_kernel(const uint32_t* keys, int nk, const int32_t* i
     }
 }
 
+// Whole sort in one CTA for small k: keys and indices in shared memory, bottom-up merge passes separated
+// by __syncthreads, then the gather of the sorted rows.
+__global__ void __launch_bounds__(1024) small_sort_kernel(const int8_t* __restrict__ rows, int k, int n_pad,
+                                                          int8_t* out) {
+    extern __shared__ __align__(16) uint32_t ss[];
+    const int nk = n_pad / 4;
+    uint32_t* keys = ss;
+    int32_t* ia = reinterpret_cast<int32_t*>(keys + (size_t)k * nk);
+    int32_t* ib = ia + k;
+    for (int t = threadIdx.x; t < k * nk; t += blockDim.x) {
+        const int r = t / nk, w = t % nk;
+        const uint8_t* g = reinterpret_cast<const uint8_t*>(rows + (size_t)r * n_pad + 4 * w);
+        keys[t] = ((uint32_t)(g[0] ^ 0x80) << 24) | ((uint32_t)(g[1] ^ 0x80) << 16) | ((uint32_t)(g[2] ^ 0x80) << 8) |
+                  (uint32_t)(g[3] ^ 0x80);
+    }
+    for (int r = threadIdx.x; r < k; r += blockDim.x) ia[r] = r;
+    __syncthreads();
+    for (int w = 1; w < k; w <<= 1) {
+        for (int p = threadIdx.x; p < k; p += blockDim.x) {
+            const int pair = p / (2 * w);
+            const int ls = pair * 2 * w, rs = min(ls + w, k), re = min(ls + 2 * w, k);
+            const int e = ia[p];
+            const uint32_t* ke = keys + (size_t)e * nk;
+            int lo, hi, off;
+            if (p < rs) {
+                lo = rs;
+                hi = re;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key_cmp(keys + (size_t)ia[mid] * nk, ke, nk) < 0) lo = mid + 1; else hi = mid;
+                }
+                off = (p - ls) + (lo - rs);
+            } else {
+                lo = ls;
+                hi = rs;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (key_cmp(keys + (size_t)ia[mid] * nk, ke, nk) <= 0) lo = mid + 1; else hi = mid;
+                }
+                off = (p - rs) + (lo - ls);
+            }
+            ib[ls + off] = e;
+        }
+        __syncthreads();
+        int32_t* t = ia;
+        ia = ib;
+        ib = t;
+    }
+    const int nw = n_pad / 16;
+    for (int t = threadIdx.x; t < k * nw; t += blockDim.x) {
+        const int r = t / nw, w = t % nw;
+        reinterpret_cast<int4*>(out + (size_t)r * n_pad)[w] = reinterpret_cast<const int4*>(rows + (size_t)ia[r] * n_pad)[w];
+    }
+}
+
 __global__ void gather_kernel(const int8_t* __restrict__ rows, const int32_t* idx, int64_t k, int n_pad, int8_t* out) {
     const int nw = n_pad / 16;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * nw; t += (int64_t)gridDim.x * blockDim.x) {
@@ -485,6 +576,14 @@ cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uin
     (void)n;
     if (k <= 0) return cudaSuccess;
     const int nk = n_pad / 4;
+    const size_t ssm = (size_t)k * nk * 4 + (size_t)k * 8;
+    if (k <= 8192 && ssm <= 160 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(small_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        if (e != cudaSuccess) return e;
+        small_sort_kernel<<<1, 1024, ssm, s>>>(rows, (int)k, n_pad, out);
+        *launches += 1;
+        return cudaGetLastError();
+    }
     sortkey_kernel<<<grid_for(k * nk), 256, 0, s>>>(rows, k, n_pad, keys, idx0);
     *launches += 1;
     int32_t* a = idx0;

@@ -82,6 +82,7 @@ struct CheckParams {
 struct FilterWork {
     int n, n_pad;
     int Lh, Wh;                   // thermometer bits per half, 32-bit words per half
+    int binary;                   // all u_i - l_i == 1: bit i of a half <-> coordinate i (fast path)
     const int32_t* off;           // n: first thermometer bit of coordinate i (prefix sum of u - l)
     const int32_t* word_c0;       // Wh: first coordinate with a bit in word w
     const int32_t* word_c1;       // Wh: last coordinate with a bit in word w
