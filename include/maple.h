@@ -139,6 +139,19 @@ void maple_dirset_free(maple_dirset* ds);
 int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32_t filter_minimal,
                            maple_dirset** out);
 
+/* ---- initial feasible solutions (NEXT #1) -------------------------------------------------------
+ * maple_feasible_starts — Eq. 4 (§4.3): projected Adam (the extraction's Adam settings) from k
+ * starts x0 ~ U(l, u) (splitmix64 counter, seed salted) on ||A x - b||^2 + lambda3 sum_i (x_i - floor x_i)
+ * (ceil x_i - x_i) over [l, u] (lambda3 = 0.1 in the paper); each final x rounded half away from zero
+ * is kept iff A x = b exactly; duplicates collapse; rows come out lexicographically sorted.
+ * b: host int32 m (right-hand side, varies per call). x_out: host int32 cap x n (out). *count receives the
+ * number of distinct feasible points found (rows beyond cap are dropped). X_debug (optional, host fp32 k x n):
+ * the final continuous iterates. "No feasible point found" is count = 0, not an error.
+ * Errors: BAD_ARG, CUDA, OOM.                                                                        */
+int maple_feasible_starts(maple_ctx* ctx, const int32_t* b, int32_t k, int32_t steps, double step_size,
+                          double lambda3, uint64_t seed, int32_t* x_out, int32_t cap, int32_t* count,
+                          float* X_debug);
+
 /* ---- augmentation -------------------------------------------------------------------------------
  * maple_augment — Graver-best augmentation (Alg. 2) from each of the k0 incumbents x0 (host,
  * k0 x n int32) in parallel, with test set D = ds ∪ -ds; each iteration takes the argmin of

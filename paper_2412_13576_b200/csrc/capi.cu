@@ -64,6 +64,7 @@ struct maple_ctx {
     // device constants
     DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, th_off, th_c0, th_c1;
     DevBuf sb_rptr, sb_rcol, sb_rval, sb_cptr, sb_crow, sb_cval, sb_lrp, sb_lr, sb_lcp, sb_lc;
+    DevBuf AT_ptr, AT_row, AT_val, fb, frows, fX;
     SparseB sb{};
     int nnz = 0, Lh = 0, Wh = 0;
     double rbound = 0;
@@ -411,6 +412,15 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         rp[r + 1] = (int32_t)col.size();
     }
     ctx->nnz = (int)col.size();
+    std::vector<int32_t> atp(n + 1, 0), atr, atv;  // CSC of A
+    for (int i = 0; i < n; ++i) {
+        for (int r = 0; r < m; ++r)
+            if (A[(size_t)r * n + i]) {
+                atr.push_back(r);
+                atv.push_back(A[(size_t)r * n + i]);
+            }
+        atp[i + 1] = (int32_t)atr.size();
+    }
     std::vector<float> bnd((size_t)n * d), bdn((size_t)d * n);
     std::vector<int8_t> b8((size_t)n * d);
     for (int i = 0; i < n; ++i)
@@ -447,6 +457,9 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->A_rowptr, rp));
     CU(upload(ctx->A_col, col));
     CU(upload(ctx->A_val, val));
+    CU(upload(ctx->AT_ptr, atp));
+    CU(upload(ctx->AT_row, atr));
+    CU(upload(ctx->AT_val, atv));
     CU(upload(ctx->dl, ctx->l));
     CU(upload(ctx->du, ctx->u));
     CU(upload(ctx->dbox, ctx->box));
@@ -454,25 +467,19 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->B_dn, bdn));
     CU(upload(ctx->B8, b8));
     CU(upload(ctx->dBp, ctx->Bp));
-    {   // sparse B (CSR, CSC) + load-balanced lane lists for the SIMT path
+    {   // sparse B (CSR, CSC; entries packed as index | int8 value << 16) + load-balanced lane lists
         std::vector<int32_t> rptr(n + 1, 0), cptr(d + 1, 0);
-        std::vector<int16_t> rcol, crow;
-        std::vector<float> rval, cval;
+        std::vector<uint32_t> rpk, cpk;
+        auto pk = [](int idx, int64_t v) { return (uint32_t)idx | ((uint32_t)(uint8_t)(int8_t)v << 16); };
         for (int i = 0; i < n; ++i) {
             for (int j = 0; j < d; ++j)
-                if (ctx->B[(size_t)i * d + j]) {
-                    rcol.push_back((int16_t)j);
-                    rval.push_back((float)ctx->B[(size_t)i * d + j]);
-                }
-            rptr[i + 1] = (int32_t)rcol.size();
+                if (ctx->B[(size_t)i * d + j]) rpk.push_back(pk(j, ctx->B[(size_t)i * d + j]));
+            rptr[i + 1] = (int32_t)rpk.size();
         }
         for (int j = 0; j < d; ++j) {
             for (int i = 0; i < n; ++i)
-                if (ctx->B[(size_t)i * d + j]) {
-                    crow.push_back((int16_t)i);
-                    cval.push_back((float)ctx->B[(size_t)i * d + j]);
-                }
-            cptr[j + 1] = (int32_t)crow.size();
+                if (ctx->B[(size_t)i * d + j]) cpk.push_back(pk(i, ctx->B[(size_t)i * d + j]));
+            cptr[j + 1] = (int32_t)cpk.size();
         }
         auto lanes = [](const std::vector<int32_t>& ptr, int cnt, std::vector<int32_t>& lp, std::vector<int32_t>& lst) {
             std::vector<int> idx(cnt);
@@ -499,29 +506,21 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         std::vector<int32_t> lrp, lr, lcp, lc;
         lanes(rptr, n, lrp, lr);
         const int mxc = lanes(cptr, d, lcp, lc);
-        const int nnzb = (int)rcol.size();
         CU(upload(ctx->sb_rptr, rptr));
-        CU(upload(ctx->sb_rcol, rcol));
-        CU(upload(ctx->sb_rval, rval));
+        CU(upload(ctx->sb_rcol, rpk));
         CU(upload(ctx->sb_cptr, cptr));
-        CU(upload(ctx->sb_crow, crow));
-        CU(upload(ctx->sb_cval, cval));
+        CU(upload(ctx->sb_crow, cpk));
         CU(upload(ctx->sb_lrp, lrp));
         CU(upload(ctx->sb_lr, lr));
         CU(upload(ctx->sb_lcp, lcp));
         CU(upload(ctx->sb_lc, lc));
         SparseB& sb = ctx->sb;
-        sb.nnz = nnzb;
+        sb.nnz = (int)rpk.size();
         sb.max_lane_cols = mxc;
-        sb.smem_bytes = (((size_t)(n + 1 + d + 1) * 4 + (size_t)nnzb * 12) + 15) & ~size_t(15);
-        const size_t per_warp = std::max<size_t>((size_t)(2 * d + n) * 4, (size_t)n * 8);
-        sb.in_smem = (sb.smem_bytes + ((per_warp + 15) & ~size_t(15)) * 8) <= 100 * 1024 ? 1 : 0;
         sb.row_ptr = ctx->sb_rptr.as<int32_t>();
-        sb.row_col = ctx->sb_rcol.as<int16_t>();
-        sb.row_val = ctx->sb_rval.as<float>();
+        sb.row_pk = ctx->sb_rcol.as<uint32_t>();
         sb.col_ptr = ctx->sb_cptr.as<int32_t>();
-        sb.col_row = ctx->sb_crow.as<int16_t>();
-        sb.col_val = ctx->sb_cval.as<float>();
+        sb.col_pk = ctx->sb_crow.as<uint32_t>();
         sb.lane_rows_ptr = ctx->sb_lrp.as<int32_t>();
         sb.lane_rows = ctx->sb_lr.as<int32_t>();
         sb.lane_cols_ptr = ctx->sb_lcp.as<int32_t>();
@@ -565,7 +564,8 @@ void maple_destroy(maple_ctx* ctx) {
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
                       &ctx->sb_rptr, &ctx->sb_rcol, &ctx->sb_rval, &ctx->sb_cptr, &ctx->sb_crow, &ctx->sb_cval,
-                      &ctx->sb_lrp, &ctx->sb_lr, &ctx->sb_lcp, &ctx->sb_lc, &ctx->step_tab, &ctx->cand,
+                      &ctx->sb_lrp, &ctx->sb_lr, &ctx->sb_lcp, &ctx->sb_lc, &ctx->AT_ptr, &ctx->AT_row,
+                      &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
@@ -958,6 +958,77 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     ctx->t_augment[1] = t;
     cudaEventElapsedTime(&t, ctx->ev[8], ctx->ev[10]);
     ctx->t_augment[2] = t;
+    return MAPLE_OK;
+}
+
+int maple_feasible_starts(maple_ctx* ctx, const int32_t* b, int32_t k, int32_t steps, double step_size,
+                          double lambda3, uint64_t seed, int32_t* x_out, int32_t cap, int32_t* count, float* X_debug) {
+    if (ctx) g_alloc_stream = ctx->stream;
+    if (!ctx || !b || !count || k < 1 || steps < 1 || !(step_size > 0) || !(lambda3 >= 0) || cap < 0 ||
+        (cap > 0 && !x_out))
+        return MAPLE_ERR_BAD_ARG;
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int n = ctx->n, m = ctx->m, np = ctx->n_pad;
+    int rc = build_step_table(ctx, steps, step_size);
+    if (rc) return rc;
+    CU(ctx->fb.ensure((size_t)m * 4));
+    CU(cudaMemcpyAsync(ctx->fb.p, b, (size_t)m * 4, cudaMemcpyHostToDevice, s));
+    CU(ctx->frows.ensure((size_t)k * np));
+    if (X_debug) CU(ctx->fX.ensure((size_t)k * n * 4));
+    rc = prepare_set(ctx, std::max<int64_t>(ctx->cand_cap, k), std::max<int64_t>(ctx->pool_cap, k));
+    if (rc) return rc;
+    FeasibleParams p{};
+    p.n = n;
+    p.m = m;
+    p.n_pad = np;
+    p.T = steps;
+    p.k = k;
+    p.lam3 = (float)lambda3;
+    p.beta1 = (float)ctx->beta1;
+    p.beta2 = (float)ctx->beta2;
+    p.eps = (float)ctx->eps;
+    p.omb1 = (float)(1.0 - ctx->beta1);
+    p.omb2 = (float)(1.0 - ctx->beta2);
+    p.step_tab = ctx->step_tab.as<float4>();
+    p.seed = seed;
+    p.A_rowptr = ctx->A_rowptr.as<int32_t>();
+    p.A_col = ctx->A_col.as<int32_t>();
+    p.A_val = ctx->A_val.as<int32_t>();
+    p.AT_colptr = ctx->AT_ptr.as<int32_t>();
+    p.AT_row = ctx->AT_row.as<int32_t>();
+    p.AT_val = ctx->AT_val.as<int32_t>();
+    p.b = ctx->fb.as<int32_t>();
+    p.lo = ctx->dl.as<int32_t>();
+    p.hi = ctx->du.as<int32_t>();
+    p.rows = ctx->frows.as<int8_t>();
+    p.cap = k;
+    p.count = counters(ctx) + C_CAND;
+    p.X_out = X_debug ? ctx->fX.as<float>() : nullptr;
+    CU(launch_feasible(p, s));
+    ctx->launches++;
+    CU(launch_dedupe(ctx->frows.as<int8_t>(), counters(ctx) + C_CAND, k, np, np, hashset(ctx), s));
+    ctx->launches++;
+    unsigned long long h[C_N];
+    rc = read_counters(ctx, h);
+    if (rc) return rc;
+    const int64_t U = (int64_t)h[C_POOL];
+    CU(ctx->tmp_rows.ensure((size_t)std::max<int64_t>(U, 1) * np));
+    CU(ctx->sortkeys.ensure((size_t)std::max<int64_t>(U, 1) * np));
+    CU(ctx->sidx0.ensure((size_t)std::max<int64_t>(U, 1) * 4));
+    CU(ctx->sidx1.ensure((size_t)std::max<int64_t>(U, 1) * 4));
+    int nl = 0;
+    CU(launch_lex_sort(ctx->pool.as<int8_t>(), U, n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
+                       ctx->sidx1.as<int32_t>(), ctx->tmp_rows.as<int8_t>(), s, &nl));
+    ctx->launches += nl;
+    std::vector<int8_t> hrows((size_t)std::max<int64_t>(U, 1) * np);
+    if (U) CU(cudaMemcpyAsync(hrows.data(), ctx->tmp_rows.p, (size_t)U * np, cudaMemcpyDeviceToHost, s));
+    if (X_debug) CU(cudaMemcpyAsync(X_debug, ctx->fX.p, (size_t)k * n * 4, cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    const int64_t w = std::min<int64_t>(U, cap);
+    for (int64_t r = 0; r < w; ++r)
+        for (int i = 0; i < n; ++i) x_out[(size_t)r * n + i] = ctx->l[i] + (int32_t)hrows[(size_t)r * np + i];
+    *count = (int32_t)U;
     return MAPLE_OK;
 }
 

@@ -13,6 +13,7 @@
 //                  r = round_half_away(z); if r changed: g = B r, keep iff g != 0 and |g| <= u - l
 //                  (P:406-407), canonical sign (first nonzero > 0), append to the candidate buffer.
 // Every reduction runs in a fixed order (CSR / CSC order), independent of placement.
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -24,122 +25,84 @@ namespace {
 
 constexpr int kWarps = 8;
 
-template <int QD>
-__global__ void __launch_bounds__(kWarps * 32, 1)
+__device__ __forceinline__ float nz_val(uint32_t e) { return (float)(int)(int8_t)(e >> 16); }
+__device__ __forceinline__ int nz_idx(uint32_t e) { return (int)(e & 0xFFFFu); }
+
+// One warp per start; the start's state (z, m, v), sign vector and rounded iterate live in the warp's slice
+// of shared memory, so registers stay few and 32 warps fit per SM (the contractions are latency-bound
+// gathers). B entries are packed (index | int8 value << 16) and read through L1.
+__global__ void __launch_bounds__(kWarps * 32)
 descent_simt_kernel(const DescentParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
     const int n = p.n, d = p.d;
     const SparseB& sb = p.sb;
-    // optional shared-memory copy of the sparse B (all warps of the block read it)
-    const int32_t* rptr = sb.row_ptr;
-    const int16_t* rcol = sb.row_col;
-    const float* rval = sb.row_val;
-    const int32_t* cptr = sb.col_ptr;
-    const int16_t* crow = sb.col_row;
-    const float* cval = sb.col_val;
-    unsigned char* wbase = smem_raw;
-    if (sb.in_smem) {
-        int32_t* s_rptr = reinterpret_cast<int32_t*>(smem_raw);
-        int32_t* s_cptr = s_rptr + (n + 1);
-        float* s_rval = reinterpret_cast<float*>(s_cptr + (d + 1));
-        float* s_cval = s_rval + sb.nnz;
-        int16_t* s_rcol = reinterpret_cast<int16_t*>(s_cval + sb.nnz);
-        int16_t* s_crow = s_rcol + sb.nnz;
-        for (int i = threadIdx.x; i <= n; i += blockDim.x) s_rptr[i] = sb.row_ptr[i];
-        for (int i = threadIdx.x; i <= d; i += blockDim.x) s_cptr[i] = sb.col_ptr[i];
-        for (int i = threadIdx.x; i < sb.nnz; i += blockDim.x) {
-            s_rval[i] = sb.row_val[i];
-            s_cval[i] = sb.col_val[i];
-            s_rcol[i] = sb.row_col[i];
-            s_crow[i] = sb.col_row[i];
-        }
-        rptr = s_rptr;
-        cptr = s_cptr;
-        rval = s_rval;
-        cval = s_cval;
-        rcol = s_rcol;
-        crow = s_crow;
-        wbase = smem_raw + sb.smem_bytes;
-        __syncthreads();
-    }
-    // per-warp scratch: z (d f32) | s (n f32, also g) | r (d f32); g0 (n f64) aliases it in the prologue
-    const size_t per_warp = ((size_t)(2 * d + n) * 4 > (size_t)n * 8 ? (size_t)(2 * d + n) * 4 : (size_t)n * 8);
+    // per-warp slice: z | m | v | r (d floats each) | s (n floats; also the g row); g0 (n doubles) aliases it
+    const size_t pw_f = (size_t)(4 * d + n) * 4, pw_d = (size_t)n * 8;
+    const size_t per_warp = pw_f > pw_d ? pw_f : pw_d;
     const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
-    unsigned char* base = wbase + per_warp_al * wid;
+    unsigned char* base = smem_raw + per_warp_al * wid;
     double* g0sh = reinterpret_cast<double*>(base);
     float* zsh = reinterpret_cast<float*>(base);
-    float* ssh = zsh + d;
-    float* rsh = ssh + n;
+    float* msh = zsh + d;
+    float* vsh = msh + d;
+    float* rsh = vsh + d;
+    float* ssh = rsh + d;
 
     const int64_t local = (int64_t)blockIdx.x * kWarps + wid;
     if (local >= p.count) return;
     const int64_t gi = p.begin + local;
-    // this lane's rows (forward / harvest) and coordinates (backward / Adam): load-balanced lists
     const int r_beg = sb.lane_rows_ptr[lane], r_end = sb.lane_rows_ptr[lane + 1];
     const int c_beg = sb.lane_cols_ptr[lane], c_end = sb.lane_cols_ptr[lane + 1];
-    int myj[QD];
-#pragma unroll
-    for (int q = 0; q < QD; ++q) myj[q] = (c_beg + q < c_end) ? sb.lane_cols[c_beg + q] : -1;
 
-    // ---- start (Alg. 3 lines 4-5) ----
-    for (int k = lane; k < n; k += 32) {
-        double U = counter_uniform(p.seed, gi, k, n);
-        g0sh[k] = start_coord(U, p.lo[k], p.hi[k]);
+    // ---- start (Alg. 3 lines 4-5): g0 in fp64, z0 = B+ g0 ----
+    for (int k = lane; k < n; k += 32) g0sh[k] = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
+    __syncwarp();
+    float z0[32];
+    const int nmine = c_end - c_beg;   // <= 32 (checked on the host)
+#pragma unroll 1
+    for (int q = 0; q < nmine; ++q) {
+        const int j = sb.lane_cols[c_beg + q];
+        double acc = 0.0;
+        const double* row = p.Bp + (size_t)j * n;
+        for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
+        if (p.Z0_out) p.Z0_out[local * d + j] = acc;
+        if (q < 32) z0[q] = (float)acc;
     }
     __syncwarp();
-    float z[QD], m[QD], v[QD];
-    int rprev[QD];
-#pragma unroll
-    for (int q = 0; q < QD; ++q) {
-        const int j = myj[q];
-        m[q] = 0.f;
-        v[q] = 0.f;
-        rprev[q] = 0x7fffffff;
-        z[q] = 0.f;
-        if (j >= 0) {
-            double acc = 0.0;
-            const double* row = p.Bp + (size_t)j * n;
-            for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
-            z[q] = (float)acc;
-            if (p.Z0_out) p.Z0_out[local * d + j] = acc;
-        }
+#pragma unroll 1
+    for (int q = 0; q < nmine; ++q) {
+        const int j = sb.lane_cols[c_beg + q];
+        zsh[j] = z0[q];
+        msh[j] = 0.f;
+        vsh[j] = 0.f;
+        rsh[j] = __int_as_float(0x7fffffff);   // "no previous round(z)": NaN never equals a rounded value
     }
     __syncwarp();
-#pragma unroll
-    for (int q = 0; q < QD; ++q)
-        if (myj[q] >= 0) zsh[myj[q]] = z[q];
-    __syncwarp();
 
-    const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2;
+    const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2;
     for (int t = 0; t < p.T; ++t) {
         // forward: y_i = sum_j B_ij z_j (CSR), s_i = sign(y_i)
         for (int a = r_beg; a < r_end; ++a) {
             const int i = sb.lane_rows[a];
             float y = 0.f;
-            for (int e = rptr[i]; e < rptr[i + 1]; ++e) y = fmaf(rval[e], zsh[rcol[e]], y);
+            for (int e = sb.row_ptr[i]; e < sb.row_ptr[i + 1]; ++e) {
+                const uint32_t w = sb.row_pk[e];
+                y = fmaf(nz_val(w), zsh[nz_idx(w)], y);
+            }
             ssh[i] = fsign(y);
         }
         __syncwarp();
-        // backward (CSC) + penalties + argmax |z|
-        float gr[QD];
+        // lowest-index argmax of |z| (λ2 term, Eq. 3)
         float best = -1.f;
         int bestj = 0x7fffffff;
-#pragma unroll
-        for (int q = 0; q < QD; ++q) {
-            const int j = myj[q];
-            gr[q] = 0.f;
-            if (j >= 0) {
-                float acc = 0.f;
-                for (int e = cptr[j]; e < cptr[j + 1]; ++e) acc = fmaf(cval[e], ssh[crow[e]], acc);
-                const float zz = z[q];
-                gr[q] = acc + p.lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
-                const float aa = fabsf(zz);
-                if (aa > best || (aa == best && j < bestj)) {
-                    best = aa;
-                    bestj = j;
-                }
+        for (int q = c_beg; q < c_end; ++q) {
+            const int j = sb.lane_cols[q];
+            const float aa = fabsf(zsh[j]);
+            if (aa > best || (aa == best && j < bestj)) {
+                best = aa;
+                bestj = j;
             }
         }
 #pragma unroll
@@ -151,55 +114,46 @@ descent_simt_kernel(const DescentParams p) {
                 bestj = oj;
             }
         }
-        if (best < 1.f) {  // lam2 term active on the lowest-index argmax coordinate
-#pragma unroll
-            for (int q = 0; q < QD; ++q) {
-                if (myj[q] == bestj) {
-                    const float zk = z[q];
-                    gr[q] += -p.lam2 * fsign(zk) / fmaxf(zk * zk, 1e-8f);
-                }
-            }
-        }
-        // Adam (reading #9)
+        // backward (CSC) + penalties + Adam (reading #9) on this lane's coordinates
         const float4 st = p.step_tab[t];
-#pragma unroll
-        for (int q = 0; q < QD; ++q) {
-            const int j = myj[q];
-            if (j >= 0) {
-                m[q] = b1 * m[q] + omb1 * gr[q];
-                v[q] = b2 * v[q] + omb2 * gr[q] * gr[q];
-                const float denom = sqrtf(v[q]) / st.y + p.eps;
-                z[q] = z[q] - st.x * m[q] / denom;
-                zsh[j] = z[q];
+        bool changed = false;
+        for (int q = c_beg; q < c_end; ++q) {
+            const int j = sb.lane_cols[q];
+            float acc = 0.f;
+            for (int e = sb.col_ptr[j]; e < sb.col_ptr[j + 1]; ++e) {
+                const uint32_t w = sb.col_pk[e];
+                acc = fmaf(nz_val(w), ssh[nz_idx(w)], acc);
+            }
+            const float zz = zsh[j];
+            float gr = acc + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
+            if (best < 1.f && j == bestj) gr += -lam2 * fsign(zz) / fmaxf(zz * zz, 1e-8f);
+            const float mm = b1 * msh[j] + omb1 * gr;
+            const float vv = b2 * vsh[j] + omb2 * gr * gr;
+            const float zn = zz - st.x * mm / (sqrtf(vv) / st.y + p.eps);
+            msh[j] = mm;
+            vsh[j] = vv;
+            zsh[j] = zn;
+            if (p.harvest) {
+                const float rn = (float)round_half_away(zn);
+                changed |= rn != rsh[j];
+                rsh[j] = rn;
             }
         }
         __syncwarp();
         if (!p.harvest) continue;
-        // harvest (Alg. 3 lines 9-10)
-        bool changed = false;
-        int r[QD];
-#pragma unroll
-        for (int q = 0; q < QD; ++q) {
-            const int j = myj[q];
-            r[q] = 0;
-            if (j >= 0) {
-                r[q] = round_half_away(z[q]);
-                changed |= (r[q] != rprev[q]);
-                rsh[j] = (float)r[q];
-            }
-        }
+        // harvest (Alg. 3 lines 9-10) when round(z) changed: g = B r (CSR), box, g != 0, canonical sign
         if (!__any_sync(0xffffffffu, changed)) continue;
-#pragma unroll
-        for (int q = 0; q < QD; ++q) rprev[q] = r[q];
-        __syncwarp();
         bool ok = true;
         for (int a = r_beg; a < r_end; ++a) {
             const int i = sb.lane_rows[a];
             float acc = 0.f;
-            for (int e = rptr[i]; e < rptr[i + 1]; ++e) acc = fmaf(rval[e], rsh[rcol[e]], acc);
+            for (int e = sb.row_ptr[i]; e < sb.row_ptr[i + 1]; ++e) {
+                const uint32_t w = sb.row_pk[e];
+                acc = fmaf(nz_val(w), rsh[nz_idx(w)], acc);
+            }
             const int gv = (int)acc;
             ok &= (abs(gv) <= p.box[i]);
-            ssh[i] = (float)gv;  // reuse s as the g row buffer
+            ssh[i] = (float)gv;  // s is dead until the next forward: reuse it as the g row
         }
         ok = __all_sync(0xffffffffu, ok);
         if (!ok) continue;
@@ -217,45 +171,30 @@ descent_simt_kernel(const DescentParams p) {
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if ((int64_t)slot < p.cand_cap) {
             int8_t* dst = p.cand + (size_t)slot * p.n_pad;
-            for (int i = lane; i < p.n_pad; i += 32)
-                dst[i] = (i < n) ? (int8_t)(firstsign * (int)ssh[i]) : (int8_t)0;
+            for (int i = lane; i < p.n_pad; i += 32) dst[i] = (i < n) ? (int8_t)(firstsign * (int)ssh[i]) : (int8_t)0;
         }
         __syncwarp();
     }
-    if (p.Z_out) {
-#pragma unroll
-        for (int q = 0; q < QD; ++q)
-            if (myj[q] >= 0) p.Z_out[local * d + myj[q]] = z[q];
-    }
-}
-
-template <int QD>
-cudaError_t launch_q(const DescentParams& p, cudaStream_t s) {
-    const int n = p.n, d = p.d;
-    const size_t per_warp = ((size_t)(2 * d + n) * 4 > (size_t)n * 8 ? (size_t)(2 * d + n) * 4 : (size_t)n * 8);
-    const size_t smem = ((per_warp + 15) & ~size_t(15)) * kWarps + (p.sb.in_smem ? p.sb.smem_bytes : 0);
-    cudaError_t e = cudaFuncSetAttribute(descent_simt_kernel<QD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t blocks = (p.count + kWarps - 1) / kWarps;
-    descent_simt_kernel<QD><<<(unsigned)blocks, kWarps * 32, smem, s>>>(p);
-    return cudaGetLastError();
+    if (p.Z_out)
+        for (int q = c_beg; q < c_end; ++q) {
+            const int j = sb.lane_cols[q];
+            p.Z_out[local * d + j] = zsh[j];
+        }
 }
 
 }  // namespace
 
 cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s) {
     if (p.count <= 0) return cudaSuccess;
-    const int qd = p.sb.max_lane_cols;
-    if (qd <= 1) return launch_q<1>(p, s);
-    if (qd <= 2) return launch_q<2>(p, s);
-    if (qd <= 4) return launch_q<4>(p, s);
-    if (qd <= 8) return launch_q<8>(p, s);
-    if (qd <= 12) return launch_q<12>(p, s);
-    if (qd <= 16) return launch_q<16>(p, s);
-    if (qd <= 24) return launch_q<24>(p, s);
-    if (qd <= 32) return launch_q<32>(p, s);
-    return cudaErrorInvalidValue;
+    if (p.sb.max_lane_cols > 32) return cudaErrorInvalidValue;
+    const int n = p.n, d = p.d;
+    const size_t per_warp = std::max<size_t>((size_t)(4 * d + n) * 4, (size_t)n * 8);
+    const size_t smem = ((per_warp + 15) & ~size_t(15)) * kWarps;
+    cudaError_t e = cudaFuncSetAttribute(descent_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (p.count + kWarps - 1) / kWarps;
+    descent_simt_kernel<<<(unsigned)blocks, kWarps * 32, smem, s>>>(p);
+    return cudaGetLastError();
 }
 
 }  // namespace maple

@@ -8,14 +8,11 @@ namespace maple {
 // Sparse B for the SIMT path: CSR (rows i, for B z and B r), CSC (columns j, for B^T s) and load-balanced
 // per-lane row / column lists (snake order by nonzero count). Column lists bound the per-lane Adam state.
 struct SparseB {
-    int nnz, in_smem, max_lane_cols;
-    size_t smem_bytes;            // bytes of the shared-memory copy (CSR + CSC)
+    int nnz, max_lane_cols;
     const int32_t* row_ptr;       // n + 1
-    const int16_t* row_col;       // nnz
-    const float* row_val;         // nnz
+    const uint32_t* row_pk;       // nnz: column index | (int8 value << 16)
     const int32_t* col_ptr;       // d + 1
-    const int16_t* col_row;       // nnz
-    const float* col_val;         // nnz
+    const uint32_t* col_pk;       // nnz: row index | (int8 value << 16)
     const int32_t* lane_rows_ptr; // 33
     const int32_t* lane_rows;     // n
     const int32_t* lane_cols_ptr; // 33
@@ -110,6 +107,29 @@ cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, const unsigne
 // keys: k * n_pad/4 uint32, idx0/idx1: k int32. Result written to out rows.
 cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uint32_t* keys, int32_t* idx0,
                             int32_t* idx1, int8_t* out, cudaStream_t s, int* launches);
+
+// ---- Eq. 4 feasible starts ----
+struct FeasibleParams {
+    int n, m, n_pad, T;
+    int64_t k;                    // number of starts
+    float lam3, beta1, beta2, eps, omb1, omb2;
+    const float4* step_tab;
+    uint64_t seed;
+    const int32_t* A_rowptr;      // CSR of A
+    const int32_t* A_col;
+    const int32_t* A_val;
+    const int32_t* AT_colptr;     // CSC of A (rows of A^T)
+    const int32_t* AT_row;
+    const int32_t* AT_val;
+    const int32_t* b;             // m
+    const int32_t* lo;            // l
+    const int32_t* hi;            // u
+    int8_t* rows;                 // kept x - l, stride n_pad
+    int64_t cap;
+    unsigned long long* count;
+    float* X_out;                 // optional debug: final iterates (k x n)
+};
+cudaError_t launch_feasible(const FeasibleParams& p, cudaStream_t s);
 
 // ---- augmentation ----
 struct AugmentParams {

@@ -62,6 +62,8 @@ _SIGS = [
     ("maple_kernel_launches", C.c_int64, [_P]),
     ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
     ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
+    ("maple_feasible_starts", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, _P,
+                                        C.c_int32, _P, _P]),
 ]
 
 
@@ -272,6 +274,17 @@ class Context:
 
     def launches(self) -> int:
         return int(_lib.maple_kernel_launches(self.h))
+
+    # ---- Eq. 4 feasible starts ----
+    def feasible_starts(self, b, k, steps, step_size, lambda3=0.1, seed=0, debug=False):
+        """maple_feasible_starts: (sorted distinct feasible points (count x n), final iterates or None)."""
+        b = np.ascontiguousarray(b, dtype=np.int32)
+        out = np.zeros((k, self.n), np.int32)
+        cnt = np.zeros(1, np.int32)
+        X = np.zeros((k, self.n), np.float32) if debug else None
+        _check(_lib.maple_feasible_starts(self.h, _ptr(b), int(k), int(steps), float(step_size), float(lambda3),
+                                          int(seed), _ptr(out), k, _ptr(cnt), _ptr(X) if debug else None), self.h)
+        return out[:min(int(cnt[0]), k)], X
 
     # ---- augmentation ----
     @staticmethod

@@ -156,8 +156,11 @@ def _identity_block(name, m, n, vals, p, gen_seed, **kw) -> Instance:
 
 
 def c3() -> Instance:
-    """configs[2]: n=300, m=20, [I_20 | W] Pi with W in {+-1, +-2} at p=0.3, binary, dense Q."""
-    return _identity_block("C3", 20, 300, [-2, -1, 1, 2], 0.3, 3, n_starts=1 << 20, steps=200, lr=0.01, seed=3)
+    """configs[2]: n=300, m=20, [I_20 | W] Pi with W in {+-1} at p=0.1 (about two constraints per free
+    variable), binary box, dense Q. (SURVEY §8(d)-1 proposed W in {+-1,+-2} at p=0.3; with that recipe no
+    binary-box kernel element is ever reached — 0 harvested by both the oracle and the GPU at T=200 — so the
+    config would measure nothing.)"""
+    return _identity_block("C3", 20, 300, [-1, 1], 0.1, 3, n_starts=1 << 20, steps=200, lr=0.01, seed=3)
 
 
 def c5() -> Instance:

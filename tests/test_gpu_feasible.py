@@ -1,0 +1,34 @@
+"""GPU parity of maple_feasible_starts (Eq. 4) with oracle/feasible.py on the same starts."""
+import numpy as np
+import pytest
+
+from oracle import feasible as F
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["C1", "C2a", "C2b"])
+def test_feasible_starts_match_oracle(gpu_lib, name):
+    from synth import config
+    inst = config(name)
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    k, T, lr = 256, 300, 0.05
+    pts, X = ctx.feasible_starts(inst.b, k, T, lr, 0.1, seed=7, debug=True)
+    assert np.all(pts @ inst.A.T == inst.b) and np.all(pts >= inst.l) and np.all(pts <= inst.u)
+    assert [tuple(r) for r in pts.tolist()] == sorted({tuple(r) for r in pts.tolist()})
+    ora, Xo = F.feasible_set(inst.A, inst.b, inst.l, inst.u, k, T, lr, seed=7)
+    # iterates: fp32 GPU vs fp64 oracle, projected Adam on a mostly convex objective
+    close = np.all(np.abs(X - Xo) <= 1e-3 * np.maximum(1, np.abs(Xo)), axis=1)
+    assert close.mean() >= 0.95
+    got = {tuple(r) for r in pts.tolist()}
+    ref = set(ora)
+    assert len(got & ref) >= 0.95 * max(1, len(got | ref))
+
+
+def test_feasible_starts_spec_examples(gpu_lib):
+    ctx = gpu_lib.Context(np.array([[1, 1]]), [0, 0], [3, 3])
+    pts, _ = ctx.feasible_starts([4], 64, 300, 0.05, seed=1)
+    assert {tuple(r) for r in pts.tolist()} <= {(1, 3), (2, 2), (3, 1)} and len(pts) >= 1
+    ctx2 = gpu_lib.Context(np.array([[2, 2]]), [0, 0], [3, 3])
+    pts, _ = ctx2.feasible_starts([3], 64, 300, 0.05, seed=1)
+    assert len(pts) == 0

@@ -1,0 +1,48 @@
+"""Pins for oracle/feasible.py — Eq. 4: SPEC worked examples S:319-330, finite differences of
+the gradient, projection invariant, and the claim of P:428 (an exact zero of Eq. 4 is a feasible point)."""
+import itertools
+
+import numpy as np
+import pytest
+
+from oracle import feasible as F
+
+
+def test_loss_examples():
+    assert F.loss([2, 2], [[1, 1]], [4]) == 0.0                       # S:319 feasible integer -> 0
+    assert F.loss([0.5], [[1]], [1]) == pytest.approx(0.275)
+    assert F.loss([1, 1], [[1, 1]], [4]) == pytest.approx(4.0)
+
+
+def test_gradient_finite_differences():
+    rng = np.random.default_rng(2)
+    for _ in range(200):
+        m, n = rng.integers(1, 4), rng.integers(2, 6)
+        A = rng.integers(-3, 4, size=(m, n))
+        b = rng.integers(-4, 5, size=m)
+        x = rng.uniform(-2, 3, size=n)
+        if np.min(np.abs(x - np.round(x))) < 1e-3:
+            continue
+        g = F.grad(x[None, :], A, b)[0]
+        h = 1e-6
+        fd = np.array([(F.loss(x + h * e, A, b) - F.loss(x - h * e, A, b)) / (2 * h) for e in np.eye(n)])
+        np.testing.assert_allclose(g, fd, rtol=1e-4, atol=1e-4)
+
+
+def test_feasible_set_examples():
+    pts, X = F.feasible_set([[1, 1]], [4], [0, 0], [3, 3], 64, 300, 0.05, seed=1)
+    assert set(pts) <= {(1, 3), (2, 2), (3, 1)} and len(pts) >= 1
+    assert F.feasible_set([[2, 2]], [3], [0, 0], [3, 3], 64, 300, 0.05, seed=1)[0] == []   # S:329 parity
+    pts, _ = F.feasible_set([[1, 2]], [5], [1, 2], [1, 2], 8, 50, 0.05, seed=1)           # S:330 l = u = x0
+    assert pts == [(1, 2)]
+    assert np.all(X >= 0) and np.all(X <= 3)                               # projection onto [l, u]
+
+
+def test_results_are_exactly_the_feasible_points_found():
+    from synth import semi_assignment
+    inst = semi_assignment(3, 4, gen_seed=3)
+    pts, _ = F.feasible_set(inst.A, inst.b, inst.l, inst.u, 128, 300, 0.05, seed=5)
+    S = {p for p in itertools.product(*[range(int(a), int(c) + 1) for a, c in zip(inst.l, inst.u)])
+         if np.all(inst.A @ np.array(p) == inst.b)}
+    assert set(pts) <= S and len(pts) > 0
+    assert pts == sorted(pts)
