@@ -281,26 +281,38 @@ def main():
     h2d = inst.A.size * 4 + inst.l.size * 4 + inst.u.size * 4 + inst.Q.size * 8 + inst.c.size * 8 + \
         inst.b.size * 4 + X0.size * 4
     d2h = 0
-    for k in range(max(2, args.steps // 2)):
+    e2e_host = []
+    # one untimed end-to-end solve first: a second context's first allocations grow the stream-ordered pool
+    # (physical pages, ~1 s at C3); later solves reuse it, as in a serving process
+    for k in range(-1, max(3, args.steps)):
         flush.fill_(3)
         sync_all()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        th = [time.perf_counter()]
         c2 = maple.Context(inst.A, inst.l, inst.u, device=local)
         c2.set_stream(stream.cuda_stream)
+        th.append(time.perf_counter())
         if world > 1:
             d2, _ = D.sharded_extract(c2, N_STARTS, T_STEPS, LR, SEED)
-            hrows = d2.rows()
+            th.append(time.perf_counter())
+            hrows = d2.rows(np.int8)
+            th.append(time.perf_counter())
             xb2, fb2 = D.sharded_augment(c2, d2, inst.Q, inst.c, inst.c0, inst.b, X0)
         else:
             d2 = c2.extract(N_STARTS, T_STEPS, LR, SEED)
-            hrows = d2.rows()
+            th.append(time.perf_counter())
+            hrows = d2.rows(np.int8)
+            th.append(time.perf_counter())
             xb2, fb2, _, _ = c2.augment(d2, inst.Q, inst.c, inst.c0, inst.b, X0)
         e1.record(stream)
         sync_all()
-        e2e_ms.append(e0.elapsed_time(e1))
-        d2h = hrows.size * 4 + xb2.size * 4 + 8
+        th.append(time.perf_counter())
+        if k >= 0:
+            e2e_ms.append(e0.elapsed_time(e1))
+            e2e_host.append(np.diff(th) * 1e3)
+        d2h = hrows.nbytes + xb2.size * 4 + 8
         d2.free()
         c2.close()
     e2e = float(np.mean(e2e_ms))
@@ -314,23 +326,30 @@ def main():
         desc_ms = float(np.mean(phase["descent"]))
         n, d = inst.n, inst.d
         units = (N_STARTS / world) * T_STEPS                      # start-steps per descent launch
+        path = ctx.descent_kernel
+        nnz_b = int(np.count_nonzero(ctx.B))
         # Dominant kernel = descent. At C2 (n=50, d=45) its two contractions are tiny tensor-core tiles and the
         # kernel is bound by the fp32 epilogue (issue/ALU). Algorithmic ALU work per start-step:
         # 16 ops per coordinate (λ1 derivative 3, gradient add 1, m 2, v 3, sqrt 1, scale+eps 1, reciprocal 1,
-        # step 2, round + change test 2) + 1 sign per row of B  ->  16 d + n.
-        alu_ops = (16.0 * d + n) * units
+        # step 2, round + change test 2) + 1 sign per row of B  ->  16 d + n. The SIMT path (sparse B, C3/C5)
+        # runs the two contractions on the fp32 lanes as well: + 2 nnz(B) FMAs.
+        ops_per = 16.0 * d + n + (2.0 * nnz_b if path == "simt" else 0.0)
+        alu_ops = ops_per * units
         achieved = alu_ops / (desc_ms * 1e-3) / 1e12
         # peak: 148 SMs x 128 fp32 lanes x sm_max_mhz (one op per lane per clock; B200_PROFILING.md unit counts)
         alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         tf32_peak = peaks.get("bf16_tflops", 1614.6) * (1.1 / 2.25)        # measured bf16 x nominal tf32 ratio
         gemm_tflops = 4.0 * n * d * units / (desc_ms * 1e-3) / 1e12       # 4nd per start-step
-        roof = {"kernel": "descent_tc_kernel", "bound": "alu", "achieved": achieved, "peak": alu_peak,
+        kname = "descent_tc_kernel" if path == "tc" else "descent_simt_kernel"
+        roof = {"kernel": kname, "bound": "alu", "achieved": achieved, "peak": alu_peak,
                 "unit": "Tops/s", "frac": achieved / alu_peak, "traffic": None,
-                "tensor_view": {"achieved_tflops": gemm_tflops, "peak_tflops_tf32": tf32_peak,
-                                "frac": gemm_tflops / tf32_peak},
-                "note": f"achieved = (16d+n) algorithmic fp32 ops x N x T / mean descent time; peak = 148 SMs x "
-                        f"128 lanes x sm_max_mhz ({src} clocks); the state never touches DRAM (ncu: "
-                        f"~140 B per launch); descent share of step {desc_ms / ms:.2f}"}
+                "ops_per_start_step": ops_per,
+                "note": f"achieved = ({'16d+n' if path == 'tc' else '16d+n+2nnz(B)'}) algorithmic fp32 ops x N x T / "
+                        f"mean descent time; peak = 148 SMs x 128 lanes x sm_max_mhz ({src} clocks); the state "
+                        f"never touches DRAM; descent share of step {desc_ms / ms:.2f}"}
+        if path == "tc":
+            roof["tensor_view"] = {"achieved_tflops": gemm_tflops, "peak_tflops_tf32": tf32_peak,
+                                   "frac": gemm_tflops / tf32_peak}
         line = {"metric": METRIC, "value": n_dirs / (ms * 1e-3), "unit": "directions/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -343,7 +362,9 @@ def main():
                 "phase_ms": {k: float(np.mean(v)) for k, v in phase.items()},
                 "start_steps_per_s": N_STARTS * T_STEPS / (float(np.mean(phase["descent"])) * 1e-3),
                 "e2e": {"value": n_dirs / (e2e * 1e-3), "unit": "directions/s", "h2d_bytes_per_step": int(h2d),
-                        "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e},
+                        "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e, "ms_all": [round(x, 3) for x in e2e_ms],
+                        "host_ms": dict(zip(["create", "extract", "rows", "augment"],
+                                            [round(float(x), 3) for x in np.median(np.array(e2e_host), axis=0)]))},
                 "gpu_launches": int(launches // max(args.steps, 1)) * args.steps,
                 "gpu_launches_per_step": launches / max(args.steps, 1),
                 "roofline": roof,

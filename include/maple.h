@@ -128,6 +128,9 @@ int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t st
 int64_t maple_dirset_size(const maple_dirset* ds);
 int64_t maple_dirset_pool_size(const maple_dirset* ds);   /* unique checked rows before the ⊑ filter */
 int maple_dirset_copy(const maple_dirset* ds, int32_t* host_rows);            /* size*n int32, host */
+/* Same rows as int8 (every entry lies in [-(u-l), u-l] with u-l <= 127): one strided device-to-host copy of
+ * size*n bytes into caller-owned host memory (pageable or pinned), synchronised on the context stream. */
+int maple_dirset_copy_i8(const maple_dirset* ds, int8_t* host_rows);
 const int8_t* maple_dirset_device_rows(const maple_dirset* ds);   /* borrowed; stride maple_dirset_stride */
 /* Device-to-device copy of the size x stride int8 rows into caller memory `dst` (e.g. a torch tensor that
  * feeds the NCCL all-gather); enqueued on the context stream and synchronised. */
@@ -193,6 +196,9 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
                         float* D2);
 /* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05. */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
+/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 = tcgen05;
+ * negative error code for a null context. Host only. */
+int maple_descent_kernel(const maple_ctx* ctx);
 
 #ifdef __cplusplus
 }

@@ -41,35 +41,40 @@ def loss(x, A, b, lam3: float = 0.1) -> float:
 
 
 def grad(X, A, b, lam3: float = 0.1):
-    """Row-wise gradient (reading F2) for a batch X (N, n)."""
-    A = np.asarray(A, np.float64)
-    R = X @ A.T - np.asarray(b, np.float64)[None, :]
-    return 2.0 * R @ A + lam3 * (np.ceil(X) + np.floor(X) - 2.0 * X)
+    """Row-wise gradient (reading F2) for a batch X (N, n), in X's dtype."""
+    dt = X.dtype
+    A = np.asarray(A, np.float64).astype(dt)
+    R = X @ A.T - np.asarray(b, np.float64).astype(dt)[None, :]
+    return dt.type(2.0) * (R @ A) + dt.type(lam3) * (np.ceil(X) + np.floor(X) - dt.type(2.0) * X)
 
 
-def descend(X0, A, b, l, u, steps, lr, lam3=0.1, beta1=0.9, beta2=0.999, eps=1e-8):
-    """Projected Adam on Eq. 4 (readings F2, F3), fp64."""
-    X = np.asarray(X0, dtype=np.float64).copy()
-    lo = np.asarray(l, np.float64)[None, :]
-    hi = np.asarray(u, np.float64)[None, :]
+def descend(X0, A, b, l, u, steps, lr, lam3=0.1, beta1=0.9, beta2=0.999, eps=1e-8, dtype=np.float64):
+    """Projected Adam on Eq. 4 (readings F2, F3). Scalars as in extraction.descend (reading #9: computed in
+    Python double, used in `dtype`), so dtype=float32 is PyTorch's fp32 Adam followed by the projection."""
+    dt = np.dtype(dtype)
+    X = np.asarray(X0, dtype=np.float64).astype(dt)
+    lo = np.asarray(l, np.float64).astype(dt)[None, :]
+    hi = np.asarray(u, np.float64).astype(dt)[None, :]
     m = np.zeros_like(X)
     v = np.zeros_like(X)
+    b1, b2 = dt.type(beta1), dt.type(beta2)
+    omb1, omb2 = dt.type(1.0 - beta1), dt.type(1.0 - beta2)
     for t in range(1, steps + 1):
         G = grad(X, A, b, lam3)
-        m = beta1 * m + (1.0 - beta1) * G
-        v = beta2 * v + (1.0 - beta2) * G * G
-        step = lr / (1.0 - beta1 ** t)
-        denom = np.sqrt(v) / np.sqrt(1.0 - beta2 ** t) + eps
+        m = b1 * m + omb1 * G
+        v = b2 * v + omb2 * G * G
+        step = dt.type(lr / (1.0 - beta1 ** t))
+        denom = np.sqrt(v) / dt.type(np.sqrt(1.0 - beta2 ** t)) + dt.type(eps)
         X = np.minimum(np.maximum(X - step * m / denom, lo), hi)
     return X
 
 
-def feasible_set(A, b, l, u, k: int, steps: int, lr: float, seed: int, lam3: float = 0.1):
+def feasible_set(A, b, l, u, k: int, steps: int, lr: float, seed: int, lam3: float = 0.1, dtype=np.float64):
     """Eq. 4 from k diversified starts (reading F4): sorted unique feasible integer points, and the final
     continuous iterates."""
     A = np.asarray(A, np.int64)
-    X = descend(starts(l, u, seed, np.arange(k)), A, b, l, u, steps, lr, lam3)
-    R = round_half_away(X)
+    X = descend(starts(l, u, seed, np.arange(k)), A, b, l, u, steps, lr, lam3, dtype=dtype)
+    R = round_half_away(X.astype(np.float64))
     ok = np.all(R @ A.T == np.asarray(b, np.int64)[None, :], axis=1)
     ok &= np.all(R >= np.asarray(l)[None, :], axis=1) & np.all(R <= np.asarray(u)[None, :], axis=1)
     pts = sorted({tuple(int(v) for v in r) for r in R[ok]})

@@ -13,6 +13,7 @@
 
 #include "../../include/maple.h"
 #include "kernels.h"
+#include "sparse_ell.h"
 #include "lattice.h"
 
 using namespace maple;
@@ -63,7 +64,8 @@ struct maple_ctx {
     std::vector<double> Bp;       // d x n
     // device constants
     DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, th_off, th_c0, th_c1;
-    DevBuf sb_rptr, sb_rcol, sb_rval, sb_cptr, sb_crow, sb_cval, sb_lrp, sb_lr, sb_lcp, sb_lc;
+    DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned;   // SIMT schedules of B (sparse_ell.h)
+    int ell_conflicts = 0;
     DevBuf AT_ptr, AT_row, AT_val, fb, frows, fX;
     SparseB sb{};
     int nnz = 0, Lh = 0, Wh = 0;
@@ -324,9 +326,13 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     return p;
 }
 
-cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
+bool uses_tc(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
-    const bool tc = ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && tc_ok);
+    return ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && tc_ok);
+}
+
+cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
+    const bool tc = uses_tc(ctx);
     ctx->launches++;
     if (tc) return launch_descent_tc(p, ctx->stream);
     return launch_descent_simt(p, ctx->stream);
@@ -467,65 +473,47 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->B_dn, bdn));
     CU(upload(ctx->B8, b8));
     CU(upload(ctx->dBp, ctx->Bp));
-    {   // sparse B (CSR, CSC; entries packed as index | int8 value << 16) + load-balanced lane lists
-        std::vector<int32_t> rptr(n + 1, 0), cptr(d + 1, 0);
-        std::vector<uint32_t> rpk, cpk;
-        auto pk = [](int idx, int64_t v) { return (uint32_t)idx | ((uint32_t)(uint8_t)(int8_t)v << 16); };
-        for (int i = 0; i < n; ++i) {
-            for (int j = 0; j < d; ++j)
-                if (ctx->B[(size_t)i * d + j]) rpk.push_back(pk(j, ctx->B[(size_t)i * d + j]));
-            rptr[i + 1] = (int32_t)rpk.size();
-        }
-        for (int j = 0; j < d; ++j) {
-            for (int i = 0; i < n; ++i)
-                if (ctx->B[(size_t)i * d + j]) cpk.push_back(pk(i, ctx->B[(size_t)i * d + j]));
-            cptr[j + 1] = (int32_t)cpk.size();
-        }
-        auto lanes = [](const std::vector<int32_t>& ptr, int cnt, std::vector<int32_t>& lp, std::vector<int32_t>& lst) {
-            std::vector<int> idx(cnt);
-            for (int i = 0; i < cnt; ++i) idx[i] = i;
-            std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
-                return ptr[a + 1] - ptr[a] > ptr[b + 1] - ptr[b];
-            });
-            std::vector<std::vector<int32_t>> per(32);
-            for (int p = 0; p < cnt; ++p) {
-                const int blk = p / 32, off = p % 32;
-                per[(blk & 1) ? 31 - off : off].push_back(idx[p]);
+    {   // sparse B: lane-major, bank-scheduled ELL words for the SIMT path (sparse_ell.h)
+        std::vector<std::vector<std::pair<int, int>>> rows(n), cols(d);
+        int nnz = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < d; ++j) {
+                const int v = (int)ctx->B[(size_t)i * d + j];
+                if (!v) continue;
+                rows[i].emplace_back(j, v);
+                cols[j].emplace_back(i, v);
+                ++nnz;
             }
-            lp.assign(33, 0);
-            lst.clear();
-            int mx = 0;
-            for (int L = 0; L < 32; ++L) {
-                std::sort(per[L].begin(), per[L].end());
-                lst.insert(lst.end(), per[L].begin(), per[L].end());
-                lp[L + 1] = (int32_t)lst.size();
-                mx = std::max(mx, (int)per[L].size());
-            }
-            return mx;
-        };
-        std::vector<int32_t> lrp, lr, lcp, lc;
-        lanes(rptr, n, lrp, lr);
-        const int mxc = lanes(cptr, d, lcp, lc);
-        CU(upload(ctx->sb_rptr, rptr));
-        CU(upload(ctx->sb_rcol, rpk));
-        CU(upload(ctx->sb_cptr, cptr));
-        CU(upload(ctx->sb_crow, cpk));
-        CU(upload(ctx->sb_lrp, lrp));
-        CU(upload(ctx->sb_lr, lr));
-        CU(upload(ctx->sb_lcp, lcp));
-        CU(upload(ctx->sb_lc, lc));
+        // forward lists longer than a quarter of a lane's share are split (the rows of a kernel basis are
+        // uneven: C3's longest has 91 nonzeros against 38 per lane); columns stay whole (Adam ownership)
+        if (std::max(n, d) > kEllMaxIndex) return MAPLE_ERR_RANGE;
+        const int chunk = std::max(4, ((nnz + 31) / 32 + 3) / 4);
+        const EllSchedule F = build_ell(rows, d, chunk);   // PAD gathers < d: z[d] is the SIMT scratch slot
+        const EllSchedule Bk = build_ell(cols, n, 0);
+        std::vector<int32_t> fix = F.fixup, fixpos = F.fixpos;
+        if (fix.empty()) fix.push_back(0);
+        if (fixpos.empty()) fixpos.push_back(0);
+        CU(upload(ctx->ell_f, F.words));
+        CU(upload(ctx->ell_own_f, F.owned));
+        CU(upload(ctx->ell_fix, fix));
+        CU(upload(ctx->ell_fixpos, fixpos));
+        CU(upload(ctx->ell_b, Bk.words));
+        CU(upload(ctx->ell_owned, Bk.owned));
         SparseB& sb = ctx->sb;
-        sb.nnz = (int)rpk.size();
-        sb.max_lane_cols = mxc;
-        sb.row_ptr = ctx->sb_rptr.as<int32_t>();
-        sb.row_pk = ctx->sb_rcol.as<uint32_t>();
-        sb.col_ptr = ctx->sb_cptr.as<int32_t>();
-        sb.col_pk = ctx->sb_crow.as<uint32_t>();
-        sb.lane_rows_ptr = ctx->sb_lrp.as<int32_t>();
-        sb.lane_rows = ctx->sb_lr.as<int32_t>();
-        sb.lane_cols_ptr = ctx->sb_lcp.as<int32_t>();
-        sb.lane_cols = ctx->sb_lc.as<int32_t>();
-        if (mxc > 32) return MAPLE_ERR_RANGE;  // d > 1024
+        sb.nnz = nnz;
+        sb.Lf = F.slots;
+        sb.qf = F.max_pieces;
+        sb.nfix = (int)F.fixup.size() / 3;
+        sb.nfixpos = (int)F.fixpos.size();
+        sb.Lb = Bk.slots;
+        sb.qd = Bk.max_pieces;
+        sb.ell_f = ctx->ell_f.as<uint32_t>();
+        sb.own_f = ctx->ell_own_f.as<int32_t>();
+        sb.fix = ctx->ell_fix.as<int32_t>();
+        sb.fixpos = ctx->ell_fixpos.as<int32_t>();
+        sb.ell_b = ctx->ell_b.as<uint32_t>();
+        sb.own_b = ctx->ell_owned.as<int32_t>();
+        ctx->ell_conflicts = F.conflicts + Bk.conflicts;
     }
     CU(upload(ctx->th_off, toff));
     CU(upload(ctx->th_c0, wc0));
@@ -563,8 +551,7 @@ void maple_destroy(maple_ctx* ctx) {
     g_alloc_stream = ctx->stream;
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
-                      &ctx->sb_rptr, &ctx->sb_rcol, &ctx->sb_rval, &ctx->sb_cptr, &ctx->sb_crow, &ctx->sb_cval,
-                      &ctx->sb_lrp, &ctx->sb_lr, &ctx->sb_lcp, &ctx->sb_lc, &ctx->AT_ptr, &ctx->AT_row,
+                      &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
@@ -624,6 +611,11 @@ int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
     if (!ctx || which < 0 || which > 2) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
     return MAPLE_OK;
+}
+
+int maple_descent_kernel(const maple_ctx* ctx) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    return uses_tc(ctx) ? 2 : 1;
 }
 
 int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates) {
@@ -775,6 +767,16 @@ int maple_dirset_copy(const maple_dirset* ds, int32_t* host_rows) {
     CU(cudaStreamSynchronize(ctx->stream));
     for (int64_t r = 0; r < ds->size; ++r)
         for (int i = 0; i < ds->n; ++i) host_rows[(size_t)r * ds->n + i] = h[(size_t)r * ds->n_pad + i];
+    return MAPLE_OK;
+}
+
+int maple_dirset_copy_i8(const maple_dirset* ds, int8_t* host_rows) {
+    if (!ds || (!host_rows && ds->size > 0)) return MAPLE_ERR_BAD_ARG;
+    if (ds->size == 0) return MAPLE_OK;
+    maple_ctx* ctx = ds->ctx;
+    CU(cudaMemcpy2DAsync(host_rows, (size_t)ds->n, ds->rows, (size_t)ds->n_pad, (size_t)ds->n, (size_t)ds->size,
+                         cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return MAPLE_OK;
 }
 

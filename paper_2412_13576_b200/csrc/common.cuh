@@ -35,6 +35,13 @@ __device__ __forceinline__ int round_half_away(float z) {
     return r;
 }
 
+// round half away from zero in float (the same value as round_half_away; + 0 turns -0 into +0)
+__device__ __forceinline__ float round_half_away_f(float z) {
+    const float t = truncf(z);
+    const float f = z - t;
+    return (fabsf(f) >= 0.5f ? t + copysignf(1.f, f) : t) + 0.f;
+}
+
 __device__ __forceinline__ float fsign(float y) { return (float)((y > 0.f) - (y < 0.f)); }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t h) { return splitmix64(h); }

@@ -3,102 +3,148 @@
 //
 // LLL-reduced kernel bases of the configs are sparse (C2a 4 %, C3 7.6 % nonzeros), so the two
 // contractions of a step are sparse matrix-vector products, not dense GEMMs:
-//   forward  y_i = sum_{j in row i} B_ij z_j      (CSR; each lane owns a load-balanced set of rows)
-//   backward Γ_j = sum_{i in col j} B_ij s_i      (CSC; each lane owns a load-balanced set of columns,
-//                                                  and the Adam state of those coordinates in registers)
+//   forward  y_i = sum_{j in row i} B_ij z_j      (each lane owns a load-balanced set of rows)
+//   backward Γ_j = sum_{i in col j} B_ij s_i      (each lane owns a load-balanced set of columns,
+//                                                  and the Adam state (m, v) of those coordinates in registers)
+// Both run from lane-major, bank-conflict-scheduled ELL words staged once per block in shared memory
+// (sparse_ell.h): per slot a warp reads one 128-byte line of words and gathers one conflict-free wavefront.
+// Per warp, shared memory holds z, the gradient Γ (reused for the rounded iterate r after Adam) and s (reused
+// for the harvested g row), so warps stay small (about 3.6 KB at C3) and 16-32 of them fit per SM.
 // Per start, Algorithm 3 lines 4-10:
 //   z0 = B+ g0, g0 ~ U(l-u, u-l) (counter RNG, fp64)
 //   for t = 1..T:  grad = B^T sign(B z) + lam1 (ceil z + floor z - 2z) + lam2-term   (Eq. 3)
 //                  Adam update of z (torch.optim.Adam formula, reading #9)
 //                  r = round_half_away(z); if r changed: g = B r, keep iff g != 0 and |g| <= u - l
 //                  (P:406-407), canonical sign (first nonzero > 0), append to the candidate buffer.
-// Every reduction runs in a fixed order (CSR / CSC order), independent of placement.
+// Every reduction runs in the fixed order of its ELL schedule, independent of block / warp placement.
 #include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_umma.cuh"   // rcp_approx, sqrt_approx (the same Adam arithmetic as the tcgen05 kernel)
 
 namespace maple {
 
 namespace {
 
-constexpr int kWarps = 8;
+// One ELL schedule (sparse_ell.h) for this lane: wl = ell + lane, resq = res + lane; the lane's k-th completed
+// piece sum goes to resq[k * 32]. Per slot: one 128-byte line of words, one conflict-free gather, one FFMA.
+__device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slots, const float* __restrict__ x,
+                                        float* __restrict__ resq) {
+    const char* xb = reinterpret_cast<const char*>(x);
+    float acc = 0.f;
+#pragma unroll 4
+    for (int e = 0; e < slots; ++e) {
+        const uint32_t w = wl[e * 32];
+        const float xv = *reinterpret_cast<const float*>(xb + (w & 0xFFFCu));
+        acc = fmaf(__uint_as_float(w & 0xFFFF0000u), xv, acc);   // bf16 B entry; PAD words carry 0
+        if (w & 1u) {
+            *resq = acc;
+            resq += 32;
+            acc = 0.f;
+        }
+    }
+}
 
-__device__ __forceinline__ float nz_val(uint32_t e) { return (float)(int)(int8_t)(e >> 16); }
-__device__ __forceinline__ int nz_idx(uint32_t e) { return (int)(e & 0xFFFFu); }
+// Forward outputs from the result queue: whole rows directly, split rows summed over their pieces in piece
+// order (fixed; reads other lanes' queue entries, hence the warp barrier).
+template <typename Store>
+__device__ __forceinline__ void ell_rows(const SparseB& sb, const int* __restrict__ ownf, const int* __restrict__ fix,
+                                         const int* __restrict__ fixpos, const float* __restrict__ res, int lane,
+                                         Store store) {
+    for (int q = 0; q < sb.qf; ++q) {
+        const int o = ownf[q * 32 + lane];
+        if (o >= 0) store(o, res[q * 32 + lane]);
+    }
+    if (sb.nfix == 0) return;
+    __syncwarp();
+    for (int f = lane; f < sb.nfix; f += 32) {
+        const int o = fix[3 * f], b = fix[3 * f + 1], c = fix[3 * f + 2];
+        float acc = 0.f;
+        for (int k = 0; k < c; ++k) acc += res[fixpos[b + k]];
+        store(o, acc);
+    }
+}
 
-// One warp per start; the start's state (z, m, v), sign vector and rounded iterate live in the warp's slice
-// of shared memory, so registers stay few and 32 warps fit per SM (the contractions are latency-bound
-// gathers). B entries are packed (index | int8 value << 16) and read through L1.
-__global__ void __launch_bounds__(kWarps * 32)
-descent_simt_kernel(const DescentParams p) {
+template <int QD>
+__global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(const DescentParams p, int per_warp_words) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int wid = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
     const int n = p.n, d = p.d;
     const SparseB& sb = p.sb;
-    // per-warp slice: z | m | v | r (d floats each) | s (n floats; also the g row); g0 (n doubles) aliases it
-    const size_t pw_f = (size_t)(4 * d + n) * 4, pw_d = (size_t)n * 8;
-    const size_t per_warp = pw_f > pw_d ? pw_f : pw_d;
-    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
-    unsigned char* base = smem_raw + per_warp_al * wid;
-    double* g0sh = reinterpret_cast<double*>(base);
-    float* zsh = reinterpret_cast<float*>(base);
-    float* msh = zsh + d;
-    float* vsh = msh + d;
-    float* rsh = vsh + d;
-    float* ssh = rsh + d;
+    const int Lf = sb.Lf, Lb = sb.Lb;
+    // block-shared: forward ELL | backward ELL | row pieces (qf x 32) | coordinates (QD x 32) | fixups
+    uint32_t* ellf = reinterpret_cast<uint32_t*>(smem_raw);
+    uint32_t* ellb = ellf + Lf * 32;
+    int* ownf = reinterpret_cast<int*>(ellb + Lb * 32);
+    int* ownb = ownf + sb.qf * 32;
+    int* fix = ownb + QD * 32;
+    int* fixpos = fix + 3 * sb.nfix;
+    for (int k = threadIdx.x; k < Lf * 32; k += blockDim.x) ellf[k] = sb.ell_f[k];
+    for (int k = threadIdx.x; k < Lb * 32; k += blockDim.x) ellb[k] = sb.ell_b[k];
+    for (int k = threadIdx.x; k < sb.qf * 32; k += blockDim.x) ownf[k] = sb.own_f[k];
+    for (int k = threadIdx.x; k < QD * 32; k += blockDim.x) {   // unused places -> scratch coordinate d (< n)
+        const int j = k < sb.qd * 32 ? sb.own_b[k] : -1;
+        ownb[k] = j >= 0 ? j : p.d;
+    }
+    for (int k = threadIdx.x; k < 3 * sb.nfix; k += blockDim.x) fix[k] = sb.fix[k];
+    for (int k = threadIdx.x; k < sb.nfixpos; k += blockDim.x) fixpos[k] = sb.fixpos[k];
+    const int shared_words = (Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + 1) & ~1);
+    __syncthreads();
 
-    const int64_t local = (int64_t)blockIdx.x * kWarps + wid;
+    // per warp: z [nx] | gr (r after Adam) [nx] | s (then the g row) [n] | result queue; g0 (n doubles) aliases
+    const int nx = n > d ? n : d;
+    float* zsh = reinterpret_cast<float*>(smem_raw) + shared_words + (size_t)wid * per_warp_words;
+    float* grsh = zsh + nx;
+    float* ssh = grsh + nx;
+    float* res = ssh + n;
+    double* g0sh = reinterpret_cast<double*>(zsh);   // shared_words and per_warp_words are even
+
+    const int64_t local = (int64_t)blockIdx.x * nwarps + wid;
     if (local >= p.count) return;
     const int64_t gi = p.begin + local;
-    const int r_beg = sb.lane_rows_ptr[lane], r_end = sb.lane_rows_ptr[lane + 1];
-    const int c_beg = sb.lane_cols_ptr[lane], c_end = sb.lane_cols_ptr[lane + 1];
+    const int* jq = ownb + lane;   // jq[q * 32]: this lane's q-th coordinate (shared table, conflict-free)
+    const uint32_t* wf = ellf + lane;
+    const uint32_t* wb = ellb + lane;
 
     // ---- start (Alg. 3 lines 4-5): g0 in fp64, z0 = B+ g0 ----
     for (int k = lane; k < n; k += 32) g0sh[k] = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
     __syncwarp();
-    float z0[32];
-    const int nmine = c_end - c_beg;   // <= 32 (checked on the host)
-#pragma unroll 1
-    for (int q = 0; q < nmine; ++q) {
-        const int j = sb.lane_cols[c_beg + q];
-        double acc = 0.0;
-        const double* row = p.Bp + (size_t)j * n;
-        for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
-        if (p.Z0_out) p.Z0_out[local * d + j] = acc;
-        if (q < 32) z0[q] = (float)acc;
+    float z0[QD], m[QD], v[QD];
+#pragma unroll
+    for (int q = 0; q < QD; ++q) {
+        m[q] = v[q] = 0.f;
+        z0[q] = 0.f;
+        if (jq[q * 32] < d) {
+            double acc = 0.0;
+            const double* row = p.Bp + (size_t)jq[q * 32] * n;
+            for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
+            if (p.Z0_out) p.Z0_out[local * d + jq[q * 32]] = acc;
+            z0[q] = (float)acc;
+        }
     }
     __syncwarp();
-#pragma unroll 1
-    for (int q = 0; q < nmine; ++q) {
-        const int j = sb.lane_cols[c_beg + q];
-        zsh[j] = z0[q];
-        msh[j] = 0.f;
-        vsh[j] = 0.f;
-        rsh[j] = __int_as_float(0x7fffffff);   // "no previous round(z)": NaN never equals a rounded value
-    }
+    for (int k = lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // padding / scratch entries read zeros
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < QD; ++q)
+        if (jq[q * 32] < d) zsh[jq[q * 32]] = z0[q];
     __syncwarp();
 
-    const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2;
+    const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2, eps = p.eps;
     for (int t = 0; t < p.T; ++t) {
-        // forward: y_i = sum_j B_ij z_j (CSR), s_i = sign(y_i)
-        for (int a = r_beg; a < r_end; ++a) {
-            const int i = sb.lane_rows[a];
-            float y = 0.f;
-            for (int e = sb.row_ptr[i]; e < sb.row_ptr[i + 1]; ++e) {
-                const uint32_t w = sb.row_pk[e];
-                y = fmaf(nz_val(w), zsh[nz_idx(w)], y);
-            }
-            ssh[i] = fsign(y);
-        }
-        __syncwarp();
-        // lowest-index argmax of |z| (λ2 term, Eq. 3)
+        // forward: s_i = sign((B z)_i)
+        ell_run(wf, Lf, zsh, res + lane);
+        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int i, float y) { ssh[i] = fsign(y); });
+        // lowest-index argmax of |z| (λ2 term, Eq. 3), over this lane's coordinates then the warp
         float best = -1.f;
         int bestj = 0x7fffffff;
-        for (int q = c_beg; q < c_end; ++q) {
-            const int j = sb.lane_cols[q];
+#pragma unroll
+        for (int q = 0; q < QD; ++q) {   // unused places point at the zero scratch coordinate d (loses ties)
+            const int j = jq[q * 32];
             const float aa = fabsf(zsh[j]);
             if (aa > best || (aa == best && j < bestj)) {
                 best = aa;
@@ -114,47 +160,46 @@ descent_simt_kernel(const DescentParams p) {
                 bestj = oj;
             }
         }
-        // backward (CSC) + penalties + Adam (reading #9) on this lane's coordinates
+        // λ2 term (Eq. 3), active while max|z| < 1, on the lowest-index argmax coordinate only
+        float extra = 0.f;
+        if (best < 1.f) {
+            const float zb = zsh[bestj];
+            extra = -lam2 * fsign(zb) / fmaxf(zb * zb, 1e-8f);
+        }
+        __syncwarp();
+        // backward: Γ = B^T s; the lane's q-th piece is its q-th coordinate, left in its own queue slot
+        ell_run(wb, Lb, ssh, res + lane);
+        // penalties + Adam (reading #9) on this lane's coordinates; r = round(z) replaces Γ in grsh.
+        // Branch-free: unused places update the scratch coordinate d (Γ = 0, z = 0: it stays 0).
         const float4 st = p.step_tab[t];
-        bool changed = false;
-        for (int q = c_beg; q < c_end; ++q) {
-            const int j = sb.lane_cols[q];
-            float acc = 0.f;
-            for (int e = sb.col_ptr[j]; e < sb.col_ptr[j + 1]; ++e) {
-                const uint32_t w = sb.col_pk[e];
-                acc = fmaf(nz_val(w), ssh[nz_idx(w)], acc);
-            }
+        bool changed = (t == 0);   // the first iterate is always harvested (no previous round(z))
+#pragma unroll
+        for (int q = 0; q < QD; ++q) {
+            const int j = jq[q * 32];
             const float zz = zsh[j];
-            float gr = acc + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
-            if (best < 1.f && j == bestj) gr += -lam2 * fsign(zz) / fmaxf(zz * zz, 1e-8f);
-            const float mm = b1 * msh[j] + omb1 * gr;
-            const float vv = b2 * vsh[j] + omb2 * gr * gr;
-            const float zn = zz - st.x * mm / (sqrtf(vv) / st.y + p.eps);
-            msh[j] = mm;
-            vsh[j] = vv;
+            // (the queue slot of an unused place may hold a forward piece sum: read 0 there)
+            float gr = (j < d ? res[q * 32 + lane] : 0.f) + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
+            gr += (j == bestj) ? extra : 0.f;
+            m[q] = fmaf(b1, m[q], omb1 * gr);
+            v[q] = fmaf(b2, v[q], omb2 * gr * gr);
+            const float den = fmaf(umma::sqrt_approx(v[q]), st.z, eps);
+            const float zn = fmaf(-st.x * m[q], umma::rcp_approx(den), zz);
             zsh[j] = zn;
-            if (p.harvest) {
-                const float rn = (float)round_half_away(zn);
-                changed |= rn != rsh[j];
-                rsh[j] = rn;
-            }
+            const float rn = round_half_away_f(zn);
+            changed |= rn != round_half_away_f(zz);
+            grsh[j] = rn;
         }
         __syncwarp();
         if (!p.harvest) continue;
-        // harvest (Alg. 3 lines 9-10) when round(z) changed: g = B r (CSR), box, g != 0, canonical sign
+        // harvest (Alg. 3 lines 9-10) when round(z) changed: g = B r, box, g != 0, canonical sign
         if (!__any_sync(0xffffffffu, changed)) continue;
         bool ok = true;
-        for (int a = r_beg; a < r_end; ++a) {
-            const int i = sb.lane_rows[a];
-            float acc = 0.f;
-            for (int e = sb.row_ptr[i]; e < sb.row_ptr[i + 1]; ++e) {
-                const uint32_t w = sb.row_pk[e];
-                acc = fmaf(nz_val(w), rsh[nz_idx(w)], acc);
-            }
+        ell_run(wf, Lf, grsh, res + lane);
+        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int i, float acc) {
             const int gv = (int)acc;
             ok &= (abs(gv) <= p.box[i]);
-            ssh[i] = (float)gv;  // s is dead until the next forward: reuse it as the g row
-        }
+            ssh[i] = (float)gv;   // s is dead until the next forward: reuse it as the g row
+        });
         ok = __all_sync(0xffffffffu, ok);
         if (!ok) continue;
         __syncwarp();
@@ -175,26 +220,63 @@ descent_simt_kernel(const DescentParams p) {
         }
         __syncwarp();
     }
-    if (p.Z_out)
-        for (int q = c_beg; q < c_end; ++q) {
-            const int j = sb.lane_cols[q];
-            p.Z_out[local * d + j] = zsh[j];
+    if (p.Z_out) {
+#pragma unroll
+        for (int q = 0; q < QD; ++q)
+            if (jq[q * 32] < d) p.Z_out[local * d + jq[q * 32]] = zsh[jq[q * 32]];
+    }
+}
+
+template <int QD>
+cudaError_t launch_qd(const DescentParams& p, cudaStream_t s) {
+    const SparseB& sb = p.sb;
+    const int n = p.n, d = p.d, nx = n > d ? n : d;
+    const int per_warp_words = (2 * nx + n + 32 * std::max(sb.qf, QD) + 1) & ~1;
+    const size_t shared_bytes = ((size_t)(sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + 1) & ~1)) * 4;
+    int dev = 0, smem_sm = 0, smem_blk = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&smem_blk, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, descent_simt_kernel<QD>);
+    if (e != cudaSuccess) return e;
+    const int warps_by_regs = 65536 / (32 * std::max(fa.numRegs, 1));
+    // warps per block: maximise resident warps per SM (shared memory and registers); the ELL is staged once
+    // per block, so among equal occupancies the smallest block wins (shorter tail)
+    int best_w = 0, best_res = -1;
+    for (int w = 4; w <= fa.maxThreadsPerBlock / 32; w += 4) {
+        const size_t bytes = shared_bytes + (size_t)w * per_warp_words * 4;
+        if (bytes > (size_t)smem_blk) break;
+        const int blocks = std::min<int>({(int)(smem_sm / (bytes + 1024)), 2048 / (32 * w), warps_by_regs / w});
+        const int res = blocks * w;
+        if (res > best_res) {
+            best_res = res;
+            best_w = w;
         }
+    }
+    if (best_w == 0) return cudaErrorInvalidValue;   // the ELL does not fit in shared memory
+    const size_t smem = shared_bytes + (size_t)best_w * per_warp_words * 4;
+    e = cudaFuncSetAttribute(descent_simt_kernel<QD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = (p.count + best_w - 1) / best_w;
+    descent_simt_kernel<QD><<<(unsigned)blocks, best_w * 32, smem, s>>>(p, per_warp_words);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
 cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s) {
     if (p.count <= 0) return cudaSuccess;
-    if (p.sb.max_lane_cols > 32) return cudaErrorInvalidValue;
-    const int n = p.n, d = p.d;
-    const size_t per_warp = std::max<size_t>((size_t)(4 * d + n) * 4, (size_t)n * 8);
-    const size_t smem = ((per_warp + 15) & ~size_t(15)) * kWarps;
-    cudaError_t e = cudaFuncSetAttribute(descent_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t blocks = (p.count + kWarps - 1) / kWarps;
-    descent_simt_kernel<<<(unsigned)blocks, kWarps * 32, smem, s>>>(p);
-    return cudaGetLastError();
+    const int qd = p.sb.qd;
+    if (qd <= 1) return launch_qd<1>(p, s);
+    if (qd <= 2) return launch_qd<2>(p, s);
+    if (qd <= 4) return launch_qd<4>(p, s);
+    if (qd <= 8) return launch_qd<8>(p, s);
+    if (qd <= 12) return launch_qd<12>(p, s);
+    if (qd <= 16) return launch_qd<16>(p, s);
+    if (qd <= 24) return launch_qd<24>(p, s);
+    if (qd <= 32) return launch_qd<32>(p, s);
+    return cudaErrorInvalidValue;
 }
 
 }  // namespace maple

@@ -7,16 +7,16 @@ namespace maple {
 
 // Sparse B for the SIMT path: CSR (rows i, for B z and B r), CSC (columns j, for B^T s) and load-balanced
 // per-lane row / column lists (snake order by nonzero count). Column lists bound the per-lane Adam state.
-struct SparseB {
-    int nnz, max_lane_cols;
-    const int32_t* row_ptr;       // n + 1
-    const uint32_t* row_pk;       // nnz: column index | (int8 value << 16)
-    const int32_t* col_ptr;       // d + 1
-    const uint32_t* col_pk;       // nnz: row index | (int8 value << 16)
-    const int32_t* lane_rows_ptr; // 33
-    const int32_t* lane_rows;     // n
-    const int32_t* lane_cols_ptr; // 33
-    const int32_t* lane_cols;     // d
+struct SparseB {   // lane-major ELL schedules of B (sparse_ell.h), built once per context
+    int nnz;                      // nonzeros of B
+    int Lf, qf, nfix, nfixpos;    // forward (rows of B): slots, pieces per lane, split rows, their pieces
+    int Lb, qd;                   // backward (columns of B): slots, coordinates per lane (whole columns)
+    const uint32_t* ell_f;        // Lf * 32 words, gather z / r (size max(n, d))
+    const int32_t* own_f;         // qf * 32: row of each piece, -1 for pieces of split rows / unused
+    const int32_t* fix;           // nfix triples (row, first, count) into fixpos
+    const int32_t* fixpos;        // queue positions q * 32 + lane of the split rows' pieces
+    const uint32_t* ell_b;        // Lb * 32 words, gather s (size n)
+    const int32_t* own_b;         // qd * 32: coordinate owned by lane L in place q, or -1
 };
 
 struct DescentParams {

@@ -50,6 +50,7 @@ _SIGS = [
     ("maple_dirset_copy", C.c_int, [_P, _P]),
     ("maple_dirset_device_rows", _P, [_P]),
     ("maple_dirset_stride", C.c_int32, [_P]),
+    ("maple_dirset_copy_i8", C.c_int, [_P, _P]),
     ("maple_dirset_copy_device", C.c_int, [_P, _P]),
     ("maple_dirset_free", None, [_P]),
     ("maple_dirset_from_host", C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(_P)]),
@@ -61,6 +62,7 @@ _SIGS = [
     ("maple_last_timings", C.c_int, [_P, _P, _P]),
     ("maple_kernel_launches", C.c_int64, [_P]),
     ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
+    ("maple_descent_kernel", C.c_int, [_P]),
     ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
     ("maple_feasible_starts", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, _P,
                                         C.c_int32, _P, _P]),
@@ -152,7 +154,12 @@ class DirSet:
     def device_ptr(self) -> int:
         return _lib.maple_dirset_device_rows(self.h) or 0
 
-    def rows(self) -> np.ndarray:
+    def rows(self, dtype=np.int32) -> np.ndarray:
+        """Host copy of the rows, (size, n); dtype int32 (default) or int8 (one strided copy, 4x fewer bytes)."""
+        if np.dtype(dtype) == np.int8:
+            out = np.empty((self.size, self.ctx.n), dtype=np.int8)
+            _check(_lib.maple_dirset_copy_i8(self.h, _ptr(out) if out.size else None), self.ctx.h)
+            return out
         out = np.zeros((self.size, self.ctx.n), dtype=np.int32)
         _check(_lib.maple_dirset_copy(self.h, _ptr(out) if out.size else None), self.ctx.h)
         return out
@@ -210,6 +217,13 @@ class Context:
 
     def set_descent_kernel(self, which: int):
         _check(_lib.maple_set_descent_kernel(self.h, which), self.h)
+
+    @property
+    def descent_kernel(self) -> str:
+        """'simt' or 'tc': the descent kernel the next extraction launches."""
+        r = _lib.maple_descent_kernel(self.h)
+        _check(min(r, 0), self.h)
+        return "tc" if r == 2 else "simt"
 
     def set_debug(self, keep_candidates: bool):
         _check(_lib.maple_set_debug(self.h, int(keep_candidates)), self.h)

@@ -17,13 +17,15 @@ def test_feasible_starts_match_oracle(gpu_lib, name):
     assert np.all(pts @ inst.A.T == inst.b) and np.all(pts >= inst.l) and np.all(pts <= inst.u)
     assert [tuple(r) for r in pts.tolist()] == sorted({tuple(r) for r in pts.tolist()})
     ora, Xo = F.feasible_set(inst.A, inst.b, inst.l, inst.u, k, T, lr, seed=7)
-    # iterates: fp32 GPU vs fp64 oracle, projected Adam on a mostly convex objective
-    close = np.all(np.abs(X - Xo) <= 1e-3 * np.maximum(1, np.abs(Xo)), axis=1)
-    assert close.mean() >= 0.95
+    # The method's output is the rounded iterate (reading F4). Projected Adam keeps oscillating around the
+    # integer points (lr 0.05), so continuous iterates differ at 1e-3 between fp32 and fp64 (C1: 45% of
+    # starts, oracle fp32 vs oracle fp64) while the rounded points agree on every start; gate on those.
+    Rg = F.round_half_away(X.astype(np.float64))
+    Ro = F.round_half_away(Xo)
+    assert np.all(Rg == Ro, axis=1).mean() >= 0.97
     got = {tuple(r) for r in pts.tolist()}
     ref = set(ora)
     assert len(got & ref) >= 0.95 * max(1, len(got | ref))
-
 
 def test_feasible_starts_spec_examples(gpu_lib):
     ctx = gpu_lib.Context(np.array([[1, 1]]), [0, 0], [3, 3])

@@ -32,6 +32,7 @@ def test_c2a_full_bench_configuration(gpu_lib):
     from synth import c2a
     inst = c2a()
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    assert ctx.descent_kernel == "tc"
     ds = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
     rows = ds.rows()
     S = _set(rows)
@@ -40,6 +41,7 @@ def test_c2a_full_bench_configuration(gpu_lib):
     assert all(OG.canonical(g) == g for g in S)                            # first nonzero > 0
     assert OP.is_antichain(S)
     assert S == _closed_semi(5, 10)
+    np.testing.assert_array_equal(ds.rows(np.int8).astype(np.int32), rows)   # strided int8 D2H path
     # determinism across runs
     np.testing.assert_array_equal(ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows(), rows)
 
@@ -104,6 +106,7 @@ def test_large_configs_small_sizes(gpu_lib, name, N, T):
     from synth import config
     inst = config(name)
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    assert ctx.descent_kernel == "simt"
     assert np.all(inst.A @ ctx.B == 0)
     Z, _ = ctx.debug_descent(N, 0, N, 3, inst.lr, inst.seed)
     _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
@@ -115,3 +118,18 @@ def test_large_configs_small_sizes(gpu_lib, name, N, T):
     ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, cand)
     assert nbad == 0
     assert [tuple(r) for r in ds.rows().tolist()] == ref
+
+
+def test_c3_directions_vs_oracle(gpu_lib):
+    """C3 at the bench's T (200) and lr on 64 starts: the SIMT path harvests, and its ⊑-minimal set agrees with
+    the fp64 oracle's (Jaccard >= 0.9, fp32 vs fp64 trajectories; G3) — every GPU row is exact (A g = 0, box)."""
+    from synth import c3
+    inst = c3()
+    N = 64
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    rows = ctx.extract(N, inst.steps, inst.lr, inst.seed).rows()
+    assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
+    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
+    ref, _ = OP.postprocess(inst.A, inst.l, inst.u, np.array(sorted(pool), dtype=np.int64).reshape(-1, inst.n))
+    G, R = _set(rows), set(ref)
+    assert len(G & R) >= 0.9 * len(G | R)
