@@ -7,11 +7,12 @@
 // Per step t (Eq. 3; Adam; harvest):
 //   MMA  G = Z B^T            kind::tf32, Z split into hi + lo TF32 terms (B is exact in TF32), fp32 accum
 //   MMA  H = round(z_{t-1}) B^T   kind::f16 (exact: small integers, fp32 accum) — the harvest expansion
-//   epi  harvest rows whose round(z) changed: g = H row, keep iff g != 0 and |g| <= u - l, canonical sign
-//   epi  S = sign(G)  (sign(0) = 0) -> f16 operand in shared memory
-//   MMA  Γ = S B             kind::f16 (exact) — the ℓ1 subgradient B^T sign(Bz)
+//   epi  (each half, its NP/2 columns) S = sign(G) -> bf16 operand; harvest test of H: box, first nonzero
+//   MMA  Γ = S B             kind::bf16 (exact) into G's TMEM columns — the ℓ1 subgradient B^T sign(Bz)
+//   epi  (overlapping that MMA) rows whose round(z) changed and whose g = H row passed both halves' tests
+//        (g != 0, |g| <= u - l): reserve a slot, each half writes its canonical-sign int8 half row
 //   epi  grad = Γ + λ1 (ceil z + floor z - 2z) + λ2 term on the lowest-index argmax |z_k| (||z||_inf < 1);
-//        Adam (torch formula) on registers; write Z_hi, Z_lo, round(z) operands for the next step.
+//        Adam (torch formula); write Z_hi, Z_lo, round(z) operands for the next step.
 // One elected thread issues every tcgen05.mma; completion is signalled through tcgen05.commit -> mbarrier.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -47,16 +48,15 @@ struct Lay {
     static constexpr uint32_t S16 = al128(R16 + kRows * DP * 2);         // 128 x NP f16 (A, backward)
     static constexpr uint32_t BOX = al128(S16 + kRows * NP * 2);         // NP f32 (u - l)
     static constexpr uint32_t PAIR = al128(BOX + NP * 4);                // pair exchange
-    static constexpr uint32_t PAIR_BYTES = 2 * 2 * kRows * 4 * 2 + 2 * kRows;
+    static constexpr uint32_t PAIR_BYTES = 2 * 2 * kRows * 4 * 2 + 2 * kRows + 2 * kRows + kRows * 8;
     static constexpr int KC = 16;                                        // g0 staging chunk (coordinates)
     static constexpr uint32_t G0_BYTES = kRows * (KC + 1) * 8;           // fp64 start staging
     static constexpr bool G0_FITS = G0_BYTES <= BOX - ZHI;
     static constexpr uint32_t G0 = G0_FITS ? ZHI : al128(PAIR + PAIR_BYTES);
     static constexpr uint32_t MBAR = al128(G0_FITS ? PAIR + PAIR_BYTES : G0 + G0_BYTES);
     static constexpr uint32_t TOTAL = MBAR + 64;
-    // TMEM columns: G | X (harvest H, then Γ) | m | v
-    static constexpr uint32_t XW = NP > DP ? NP : DP;
-    static constexpr uint32_t CG = 0, CX = NP, CM = NP + XW, CV = NP + XW + DP;
+    // TMEM columns: G (then Γ, DP <= NP) | H (harvest) | m | v
+    static constexpr uint32_t CG = 0, CX = NP, CM = 2 * NP, CV = 2 * NP + DP;
     static_assert(CV + DP <= kTmemCols, "TMEM budget");
 };
 
@@ -87,6 +87,8 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
     float* amax = reinterpret_cast<float*>(sm + L::PAIR);             // [parity][half][row]
     int* aidx = reinterpret_cast<int*>(amax + 2 * 2 * kRows);         // [parity][half][row]
     uint8_t* chg = reinterpret_cast<uint8_t*>(aidx + 2 * 2 * kRows);  // [half][row]
+    int8_t* hx = reinterpret_cast<int8_t*>(chg + 2 * kRows);           // [half][row]: harvest test, see below
+    unsigned long long* slot_sh = reinterpret_cast<unsigned long long*>(hx + 2 * kRows);   // [row]
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + L::MBAR);
     uint32_t* tbase_sh = reinterpret_cast<uint32_t*>(mbar + 2);
     float* boxs = reinterpret_cast<float*>(sm + L::BOX);
@@ -226,80 +228,60 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
         mbar_wait(&mbar[0], phA);
         phA ^= 1;
         fence_after();
-        if (half == 0) {
-            // ---- harvest of z_{t-1} (half 0, all NP columns of H): rows whose round(z) changed ----
-            if (do_harv) {
-                const uint8_t cf = chg[row] | chg[kRows + row];
-                const bool row_chg = active && cf == 1;
-                if (__any_sync(0xffffffffu, row_chg)) {
-                    // pass 1: box test and canonical sign (first nonzero) of g = H row
-                    auto pack4 = [&](const uint32_t* r4) {       // 4 exact small-integer floats -> 4 int8
-                        uint32_t bq[4];
+        constexpr int NH = NP / 2;
+        constexpr int CW = NH % 16 == 0 ? 16 : 8;   // columns per TMEM load batch (NH is a multiple of 8)
+        const int c_lo = half * NH;   // this thread's column half of G, H and the candidate row
+        // 4 exact small-integer floats -> 4 int8 bytes (low byte of the 1.5 * 2^23 magic sum)
+        auto pack4 = [&](const uint32_t* r4) {
+            uint32_t bq[4];
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) bq[e] = __float_as_uint(__uint_as_float(r4[e]) + 12582912.f);
-                        return __byte_perm(__byte_perm(bq[0], bq[1], 0x0040), __byte_perm(bq[2], bq[3], 0x0040),
-                                           0x5410);
-                    };
-                    bool ok = true;
-                    int sgn = 0;
+            for (int e = 0; e < 4; ++e) bq[e] = __float_as_uint(__uint_as_float(r4[e]) + 12582912.f);
+            return __byte_perm(__byte_perm(bq[0], bq[1], 0x0040), __byte_perm(bq[2], bq[3], 0x0040), 0x5410);
+        };
+        const bool row_chg = do_harv && active && (chg[row] | chg[kRows + row]) == 1;
+        const bool warp_harv = __any_sync(0xffffffffu, row_chg);
+        if (do_harv) {
+            // ---- harvest test of g = H row (z_{t-1}), this half's columns: box |g| <= u - l and the sign of
+            // the first nonzero. hx = 0: fails the box; 1: in the box, all zero here; 2 / 3: first nonzero > 0 / < 0
+            int8_t code = 1;
+            if (warp_harv) {
+                bool ok = true;
+                int sgn = 0;
 #pragma unroll
-                    for (int c0 = 0; c0 < NP; c0 += 16) {
-                        uint32_t r[16];
-                        ld8(tl + L::CX + c0, &r[0]);
-                        ld8(tl + L::CX + c0 + 8, &r[8]);
-                        wait8(&r[0]);
-                        wait8(&r[8]);
+                for (int c0 = 0; c0 < NH; c0 += CW) {
+                    uint32_t r[CW];
+                    ld8(tl + L::CX + c_lo + c0, &r[0]);
+                    if constexpr (CW == 16) ld8(tl + L::CX + c_lo + c0 + 8, &r[8]);
+                    wait8(&r[0]);
+                    if constexpr (CW == 16) wait8(&r[8]);
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                            for (int e = 0; e < 4; ++e) ok &= fabsf(__uint_as_float(r[4 * q + e])) <= boxs[c0 + 4 * q + e];
-                            const uint32_t w = pack4(&r[4 * q]);
-                            if (sgn == 0 && w != 0u) sgn = ((int8_t)(w >> (8 * ((__ffs(w) - 1) >> 3)))) > 0 ? 1 : -1;
-                        }
-                    }
-                    const bool want = row_chg && ok && sgn != 0;
-                    const unsigned mask = __ballot_sync(0xffffffffu, want);
-                    if (mask) {
-                        // pass 2: reserve slots (one atomic per warp) and write the canonical int8 rows
-                        const int leader = __ffs(mask) - 1;
-                        unsigned long long base = 0;
-                        if (lane == leader) base = atomicAdd(p.cand_count, (unsigned long long)__popc(mask));
-                        base = __shfl_sync(0xffffffffu, base, leader);
-                        const unsigned long long slot = base + __popc(mask & ((1u << lane) - 1u));
-                        uint4* dst = reinterpret_cast<uint4*>(p.cand + (size_t)slot * p.n_pad);
-                        const bool store = want && (int64_t)slot < cap;
-#pragma unroll
-                        for (int c0 = 0; c0 < NP; c0 += 16) {
-                            uint32_t r[16];
-                            ld8(tl + L::CX + c0, &r[0]);
-                            ld8(tl + L::CX + c0 + 8, &r[8]);
-                            wait8(&r[0]);
-                            wait8(&r[8]);
-                            uint4 w = make_uint4(pack4(&r[0]), pack4(&r[4]), pack4(&r[8]), pack4(&r[12]));
-                            if (sgn < 0) {
-                                w.x = __vneg4(w.x);
-                                w.y = __vneg4(w.y);
-                                w.z = __vneg4(w.z);
-                                w.w = __vneg4(w.w);
-                            }
-                            if (store) dst[c0 / 16] = w;
-                        }
+                    for (int q = 0; q < CW / 4; ++q) {
+                        const float4 bx = *reinterpret_cast<const float4*>(boxs + c_lo + c0 + 4 * q);   // broadcast
+                        ok &= fabsf(__uint_as_float(r[4 * q + 0])) <= bx.x;
+                        ok &= fabsf(__uint_as_float(r[4 * q + 1])) <= bx.y;
+                        ok &= fabsf(__uint_as_float(r[4 * q + 2])) <= bx.z;
+                        ok &= fabsf(__uint_as_float(r[4 * q + 3])) <= bx.w;
+                        const uint32_t w = pack4(&r[4 * q]);
+                        if (sgn == 0 && w != 0u) sgn = ((int8_t)(w >> (8 * ((__ffs(w) - 1) >> 3)))) > 0 ? 1 : -1;
                     }
                 }
+                code = !ok ? 0 : (sgn == 0 ? 1 : (sgn > 0 ? 2 : 3));
             }
-        } else if (do_fwd) {
-            // ---- S = sign(B z) (half 1, all NP columns of G) -> bf16 backward operand ----
+            hx[half * kRows + row] = code;
+        }
+        if (do_fwd) {
+            // ---- S = sign(B z), this half's columns of G -> bf16 backward operand ----
             // sign via bf16 pairs: rounding to bf16 never flips a sign and has fp32's exponent range
             const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
 #pragma unroll
-            for (int c0 = 0; c0 < NP; c0 += 16) {
-                uint32_t r[16];
-                ld8(tl + L::CG + c0, &r[0]);
-                ld8(tl + L::CG + c0 + 8, &r[8]);
+            for (int c0 = 0; c0 < NH; c0 += CW) {
+                uint32_t r[CW];
+                ld8(tl + L::CG + c_lo + c0, &r[0]);
+                if constexpr (CW == 16) ld8(tl + L::CG + c_lo + c0 + 8, &r[8]);
                 wait8(&r[0]);
-                wait8(&r[8]);
+                if constexpr (CW == 16) wait8(&r[8]);
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
+                for (int c = 0; c < CW / 8; ++c) {
                     uint4 w;
                     uint32_t* wp = &w.x;
 #pragma unroll
@@ -309,22 +291,54 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                         const __nv_bfloat162 sg = __hsub2(__hgt2(h, zero2), __hlt2(h, zero2));
                         wp[e] = *reinterpret_cast<const uint32_t*>(&sg);
                     }
-                    *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, c0 / 8 + c, kRows)) = w;
+                    *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, (c_lo + c0) / 8 + c, kRows)) = w;
+                }
+            }
+        }
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();  // B2: S and both halves' harvest tests written; G consumed (Γ reuses its columns)
+        if (do_fwd && tid == 0) {
+            fence_after();
+#pragma unroll
+            for (int kk = 0; kk < NP / 16; ++kk)
+                mma_f16(tbase + L::CG, desc(sS + kk * 2 * LBO_A, LBO_A, SBO), desc(sBT + kk * 2 * LBO_D, LBO_D, SBO),
+                        ID_BWD, kk > 0);
+            commit(&mbar[1]);
+        }
+        if (do_harv && warp_harv) {
+            // ---- candidate rows (overlaps the backward MMA): both halves passed the box test, g != 0 ----
+            const int8_t h0 = hx[row], h1 = hx[kRows + row];
+            const int code = h0 >= 2 ? h0 : h1;   // the first nonzero lies in half 0 if half 0 has one
+            const bool want = row_chg && h0 != 0 && h1 != 0 && code >= 2;
+            const unsigned mask = __ballot_sync(0xffffffffu, want);   // identical in both halves' warps
+            if (mask) {
+                if (half == 0) {   // one atomic per warp pair; the slot goes to the partner warp via shared memory
+                    const int leader = __ffs(mask) - 1;
+                    unsigned long long base = 0;
+                    if (lane == leader) base = atomicAdd(p.cand_count, (unsigned long long)__popc(mask));
+                    base = __shfl_sync(0xffffffffu, base, leader);
+                    slot_sh[row] = base + __popc(mask & ((1u << lane) - 1u));
+                }
+                bar_sync_pair(quad);   // warps quad and quad + 4
+                const unsigned long long slot = slot_sh[row];
+                const bool store = want && (int64_t)slot < cap;
+                int8_t* dst = p.cand + (size_t)slot * p.n_pad + c_lo;   // 8-byte aligned (n_pad, NH % 8 == 0)
+#pragma unroll
+                for (int c0 = 0; c0 < NH; c0 += 8) {
+                    uint32_t r[8];
+                    ld8(tl + L::CX + c_lo + c0, &r[0]);   // tcgen05.ld is warp-collective: every lane loads
+                    wait8(&r[0]);
+                    uint2 w = make_uint2(pack4(&r[0]), pack4(&r[4]));
+                    if (code == 3) {
+                        w.x = __vneg4(w.x);
+                        w.y = __vneg4(w.y);
+                    }
+                    if (store) *reinterpret_cast<uint2*>(dst + c0) = w;
                 }
             }
         }
         if (!do_fwd) break;
-        fence_proxy_async();
-        fence_before();
-        __syncthreads();  // B2: S written; H consumed (its TMEM columns are reused by Γ)
-        if (tid == 0) {
-            fence_after();
-#pragma unroll
-            for (int kk = 0; kk < NP / 16; ++kk)
-                mma_f16(tbase + L::CX, desc(sS + kk * 2 * LBO_A, LBO_A, SBO), desc(sBT + kk * 2 * LBO_D, LBO_D, SBO),
-                        ID_BWD, kk > 0);
-            commit(&mbar[1]);
-        }
         mbar_wait(&mbar[1], phB);
         phB ^= 1;
         fence_after();
@@ -355,7 +369,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
 #pragma unroll
             for (int c = 0; c < DH / 8; ++c) {
                 uint32_t rg[8], rm[8], rv[8];
-                ld8(tl + L::CX + half * DH + 8 * c, rg);
+                ld8(tl + L::CG + half * DH + 8 * c, rg);
                 ld8(tl + L::CM + half * DH + 8 * c, rm);
                 ld8(tl + L::CV + half * DH + 8 * c, rv);
                 // current iterate z = Z_hi + Z_lo and r = round(z) (the f16 harvest operand written last step)

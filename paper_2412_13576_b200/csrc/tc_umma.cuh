@@ -120,6 +120,16 @@ __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.
 __device__ __forceinline__ float tf32_rna(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
+// named barrier 1 + q (q = 0..3) over 64 threads, with immediate ids so ptxas reserves only those
+__device__ __forceinline__ void bar_sync_pair(int q) {
+    switch (q) {
+        case 0: asm volatile("bar.sync 1, 64;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+        default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+    }
+}
+
 __device__ __forceinline__ float rcp_approx(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
