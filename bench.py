@@ -58,6 +58,19 @@ def _peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _traffic(kernel, n_starts):
+    """dram read + write bytes per launch of `kernel` from the committed ncu --set full capture (profiles/
+    r1_traffic.json) when it was taken on this workload and start count, else None."""
+    try:
+        t = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")))
+        e = t[kernel]
+        if e["workload"] == WORKLOAD and e["n_starts"] == n_starts:
+            return e["read_bytes"] + e["write_bytes"]
+    except (OSError, KeyError, ValueError):
+        pass
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -334,20 +347,22 @@ def main():
         # step 2, round + change test 2) + 1 sign per row of B  ->  16 d + n. The SIMT path (sparse B, C3/C5)
         # runs the two contractions on the fp32 lanes as well: + 2 nnz(B) FMAs.
         ops_per = 16.0 * d + n + (2.0 * nnz_b if path == "simt" else 0.0)
+        tc_path = path in ("tc", "tc4")
         alu_ops = ops_per * units
         achieved = alu_ops / (desc_ms * 1e-3) / 1e12
         # peak: 148 SMs x 128 fp32 lanes x sm_max_mhz (one op per lane per clock; B200_PROFILING.md unit counts)
         alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
         tf32_peak = peaks.get("bf16_tflops", 1614.6) * (1.1 / 2.25)        # measured bf16 x nominal tf32 ratio
         gemm_tflops = 4.0 * n * d * units / (desc_ms * 1e-3) / 1e12       # 4nd per start-step
-        kname = "descent_tc_kernel" if path == "tc" else "descent_simt_kernel"
+        kname = {"tc": "descent_tc_kernel", "tc4": "descent_tc4_kernel"}.get(path, "descent_simt_kernel")
         roof = {"kernel": kname, "bound": "alu", "achieved": achieved, "peak": alu_peak,
-                "unit": "Tops/s", "frac": achieved / alu_peak, "traffic": None,
+                "unit": "Tops/s", "frac": achieved / alu_peak, "traffic": _traffic(kname, N_STARTS // world),
                 "ops_per_start_step": ops_per,
-                "note": f"achieved = ({'16d+n' if path == 'tc' else '16d+n+2nnz(B)'}) algorithmic fp32 ops x N x T / "
+                "note": f"achieved = ({'16d+n' if tc_path else '16d+n+2nnz(B)'}) algorithmic fp32 ops x N x T / "
                         f"mean descent time; peak = 148 SMs x 128 lanes x sm_max_mhz ({src} clocks); the state "
-                        f"never touches DRAM; descent share of step {desc_ms / ms:.2f}"}
-        if path == "tc":
+                        f"never touches DRAM (traffic: B, B+ reads and the harvested candidate rows, from the ncu capture in "
+                        f"profiles/); descent share of step {desc_ms / ms:.2f}"}
+        if tc_path:
             roof["tensor_view"] = {"achieved_tflops": gemm_tflops, "peak_tflops_tf32": tf32_peak,
                                    "frac": gemm_tflops / tf32_peak}
         line = {"metric": METRIC, "value": n_dirs / (ms * 1e-3), "unit": "directions/s", "n_gpus": world,

@@ -194,9 +194,10 @@ int64_t maple_kernel_launches(const maple_ctx* ctx);
  * descriptors as the descent kernel; the caller compares with an exact host product. */
 int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1, const float* A2, const float* B2,
                         float* D2);
-/* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05. */
+/* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05 with 2 threads per
+ * start, 3 = tcgen05 with 4 threads per start (2 and 3 compute the same iterates). */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
-/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 = tcgen05;
+/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05;
  * negative error code for a null context. Host only. */
 int maple_descent_kernel(const maple_ctx* ctx);
 

@@ -326,16 +326,22 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     return p;
 }
 
-bool uses_tc(const maple_ctx* ctx) {
+constexpr int kAutoTc = 2;   // auto choice for tensor-core shapes
+
+// the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start)
+int which_descent(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
-    return ctx->descent_kernel == 2 || (ctx->descent_kernel == 0 && tc_ok);
+    if (ctx->descent_kernel != 0) return ctx->descent_kernel;
+    return tc_ok ? kAutoTc : 1;
 }
 
 cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
-    const bool tc = uses_tc(ctx);
     ctx->launches++;
-    if (tc) return launch_descent_tc(p, ctx->stream);
-    return launch_descent_simt(p, ctx->stream);
+    switch (which_descent(ctx)) {
+        case 2: return launch_descent_tc(p, ctx->stream);
+        case 3: return launch_descent_tc4(p, ctx->stream);
+        default: return launch_descent_simt(p, ctx->stream);
+    }
 }
 
 int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps, double lr) {
@@ -344,7 +350,7 @@ int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t 
     if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
     if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
     if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
-    if (ctx->descent_kernel == 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
+    if (ctx->descent_kernel >= 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
         FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
     return MAPLE_OK;
 }
@@ -608,14 +614,14 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
 }
 
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
-    if (!ctx || which < 0 || which > 2) return MAPLE_ERR_BAD_ARG;
+    if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
     return MAPLE_OK;
 }
 
 int maple_descent_kernel(const maple_ctx* ctx) {
     if (!ctx) return MAPLE_ERR_BAD_ARG;
-    return uses_tc(ctx) ? 2 : 1;
+    return which_descent(ctx);
 }
 
 int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates) {

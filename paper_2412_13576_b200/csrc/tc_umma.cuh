@@ -114,6 +114,21 @@ __device__ __forceinline__ void st8(uint32_t taddr, const uint32_t* r) {
                  "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                  : "memory");
 }
+// 4-column variants (32 lanes x 32 bit, 4 consecutive columns per thread)
+__device__ __forceinline__ void ld4(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(taddr));
+}
+__device__ __forceinline__ void wait4(uint32_t* r) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]) : : "memory");
+}
+__device__ __forceinline__ void st4(uint32_t taddr, const uint32_t* r) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+                 "r"(r[2]), "r"(r[3])
+                 : "memory");
+}
+
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // round-to-nearest (ties away) to TF32 with integer ops: identical to cvt.rna.tf32.f32 for finite x
@@ -127,6 +142,16 @@ __device__ __forceinline__ void bar_sync_pair(int q) {
         case 1: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
         case 2: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
         default: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+    }
+}
+
+// named barrier 1 + q (q = 0..3) over 128 threads (the four warps q, q + 4, q + 8, q + 12)
+__device__ __forceinline__ void bar_sync_quad(int q) {
+    switch (q) {
+        case 0: asm volatile("bar.sync 1, 128;" ::: "memory"); break;
+        case 1: asm volatile("bar.sync 2, 128;" ::: "memory"); break;
+        case 2: asm volatile("bar.sync 3, 128;" ::: "memory"); break;
+        default: asm volatile("bar.sync 4, 128;" ::: "memory"); break;
     }
 }
 

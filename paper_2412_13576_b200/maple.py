@@ -220,10 +220,10 @@ class Context:
 
     @property
     def descent_kernel(self) -> str:
-        """'simt' or 'tc': the descent kernel the next extraction launches."""
+        """'simt', 'tc' or 'tc4': the descent kernel the next extraction launches."""
         r = _lib.maple_descent_kernel(self.h)
         _check(min(r, 0), self.h)
-        return "tc" if r == 2 else "simt"
+        return {1: "simt", 2: "tc", 3: "tc4"}[r]
 
     def set_debug(self, keep_candidates: bool):
         _check(_lib.maple_set_debug(self.h, int(keep_candidates)), self.h)

@@ -32,7 +32,7 @@ def test_c2a_full_bench_configuration(gpu_lib):
     from synth import c2a
     inst = c2a()
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
-    assert ctx.descent_kernel == "tc"
+    assert ctx.descent_kernel in ("tc", "tc4")
     ds = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
     rows = ds.rows()
     S = _set(rows)
