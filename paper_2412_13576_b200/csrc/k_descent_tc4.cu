@@ -49,8 +49,8 @@ struct Lay4 {
     static constexpr uint32_t R16 = al128(ZLO + kRows * DP * 4);         // 128 x DP f16 (A, harvest)
     static constexpr uint32_t S16 = al128(R16 + kRows * DP * 2);         // 128 x NP bf16 (A, backward)
     static constexpr uint32_t BOX = al128(S16 + kRows * NP * 2);         // NP f32 (u - l)
-    static constexpr uint32_t PAIR = al128(BOX + NP * 4);                // amax | chg | hx | slots
-    static constexpr uint32_t PAIR_BYTES = 2 * kParts * kRows * 4 + kRows * 4 + kRows * 4 + kRows * 8;
+    static constexpr uint32_t PAIR = al128(BOX + NP * 4);                // amax | aidx | chg | hx | slots
+    static constexpr uint32_t PAIR_BYTES = 2 * 2 * kParts * kRows * 4 + kRows * 4 + kRows * 4 + kRows * 8;
     static constexpr int KC = 16;                                        // g0 staging chunk (coordinates)
     static constexpr uint32_t G0_BYTES = kRows * (KC + 1) * 8;           // fp64 start staging
     static constexpr bool G0_FITS = G0_BYTES <= BOX - ZHI;
@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
     const int n = p.n, d = p.d;
 
     float* amax = reinterpret_cast<float*>(sm + L::PAIR);                     // [parity][part][row]
-    uint32_t* chg = reinterpret_cast<uint32_t*>(amax + 2 * kParts * kRows);   // [row], byte `part`: change flags
+    int* aidx = reinterpret_cast<int*>(amax + 2 * kParts * kRows);            // [parity][part][row]: first argmax
+    uint32_t* chg = reinterpret_cast<uint32_t*>(aidx + 2 * kParts * kRows);   // [row], byte `part`: change flags
     uint32_t* hx = chg + kRows;                                               // [row], byte `part`: harvest test
     unsigned long long* slot_sh = reinterpret_cast<unsigned long long*>(hx + kRows);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + L::MBAR);
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
     // Z_lo = z - Z_hi, so z = Z_hi + Z_lo exactly. Also round(z) as f16 (the harvest operand).
     {
         float lmax = -1.f;
+        int lq = 0;
 #pragma unroll
         for (int c = 0; c < DQ / 4; ++c) {
             const int col = part * DQ + 4 * c;
@@ -158,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
                 const float rq = fabsf(dq) >= 0.5f ? tq + copysignf(1.f, dq) : tq;
                 const uint32_t hb = __half_as_ushort(__float2half_rn(rq));
                 rn[e >> 1] |= (e & 1) ? (hb << 16) : hb;
-                lmax = fmaxf(lmax, fabsf(zz));
+                if (fabsf(zz) > lmax) {
+                    lmax = fabsf(zz);
+                    lq = q;
+                }
             }
             const uint32_t off = op_offset(row, col >> 2, kRows);
             *reinterpret_cast<float4*>(sm + L::ZHI + off) = hi;
@@ -167,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
                 make_uint2(rn[0], rn[1]);
         }
         amax[(0 * kParts + part) * kRows + row] = lmax;
+        aidx[(0 * kParts + part) * kRows + row] = lq;
     }
 
     const uint32_t sZHI = smem_u32(sm + L::ZHI), sZLO = smem_u32(sm + L::ZLO), sR = smem_u32(sm + L::R16);
@@ -215,8 +221,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
             }
             commit(&mbar[0]);
         }
-        mbar_wait(&mbar[0], phA);
+        // one warp polls the mbarrier; the others wait in the CTA barrier without issuing
+        if (warp == 0) mbar_wait(&mbar[0], phA);
         phA ^= 1;
+        __syncthreads();
         fence_after();
         // change flags of z_{t-1}, all four parts: bit 0 round(z) changed, bit 1 max |z| > 2047.5 (see below)
         const uint32_t cw = chg[row];
@@ -314,8 +322,9 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
             }
         }
         if (!do_fwd) break;
-        mbar_wait(&mbar[1], phB);
+        if (warp == 0) mbar_wait(&mbar[1], phB);
         phB ^= 1;
+        __syncthreads();
         fence_after();
         // ---- gradient of Eq. 3 + Adam, this thread's DQ coordinates, 4 at a time ----
         const int par = (t - 1) & 1;
@@ -332,22 +341,18 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
         // λ2 term of Eq. 3 while ||z||_inf < 1, on the lowest-index argmax coordinate (found by its owner part)
         int kq = -1;
         float extra = 0.f;
-        if (zinf < 1.f && part == own) {
-            for (int q = 0; q < DQ; ++q) {
-                const int j = part * DQ + q;
-                const uint32_t off = op_offset(row, j >> 2, kRows) + (j & 3) * 4;
-                const float zq = *reinterpret_cast<const float*>(sm + L::ZHI + off) +
-                                 *reinterpret_cast<const float*>(sm + L::ZLO + off);
-                if (fabsf(zq) == zinf) {
-                    kq = q;
-                    if (zq != 0.f) extra = -lam2 * copysignf(1.f, zq) / fmaxf(zq * zq, 1e-8f);
-                    break;
-                }
-            }
+        if (zinf < 1.f && part == own) {   // the owning part's recorded first argmax
+            kq = aidx[(par * kParts + part) * kRows + row];
+            const int j = part * DQ + kq;
+            const uint32_t off = op_offset(row, j >> 2, kRows) + (j & 3) * 4;
+            const float zq = *reinterpret_cast<const float*>(sm + L::ZHI + off) +
+                             *reinterpret_cast<const float*>(sm + L::ZLO + off);
+            if (zq != 0.f) extra = -lam2 * copysignf(1.f, zq) / fmaxf(zq * zq, 1e-8f);
         }
         const float4 st = p.step_tab[t - 1];     // (lr / (1 - b1^t), -, 1 / sqrt(1 - b2^t))
         bool ch = (t == 1);
-        float lmax = 0.f;
+        float lmax = 0.f;   // max |z_new| over this part and its first index (strict >: lowest index wins)
+        int lq = 0;
         auto adam = [&](auto has_extra) {
 #pragma unroll
             for (int c = 0; c < DQ / 4; ++c) {
@@ -390,7 +395,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
                     const float dn = zn - tn;
                     // round half away from zero; + 0 turns -0 into +0 so equal values have equal f16 bits
                     rn4[e] = (fabsf(dn) >= 0.5f ? tn + copysignf(1.f, dn) : tn) + 0.f;
-                    lmax = fmaxf(lmax, fabsf(zn));
+                    if (fabsf(zn) > lmax) {
+                        lmax = fabsf(zn);
+                        lq = q;
+                    }
                     hz = tf32_rna(zn);
                     lz = zn - hz;
                 }
@@ -412,6 +420,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
             adam(std::integral_constant<bool, false>());
         st_wait();
         amax[((t & 1) * kParts + part) * kRows + row] = lmax;
+        aidx[((t & 1) * kParts + part) * kRows + row] = lq;
         // bit 0: round(z) changed; bit 1: max |z| > 2047.5, i.e. round(z) may leave the exact f16 range of the
         // harvest operand. The host selects this kernel only when every in-box g has |B+ g|_inf < 2047, so such
         // an iterate cannot map to a g inside the box and skipping it is exact.
