@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if src.endswith(".cu"):
                 jobs.append([NVCC] + NVFLAGS + ["-c", s, "-o", o])
             else:
-                jobs.append(["g++", "-std=c++17", "-O2", "-fPIC", "-c", s, "-o", o])
+                jobs.append(["g++", "-std=c++17", "-O3", "-fPIC", "-c", s, "-o", o])
     logs = []
     with ThreadPoolExecutor(max_workers=max(1, min(8, len(jobs)))) as ex:
         logs = list(ex.map(_run, jobs))

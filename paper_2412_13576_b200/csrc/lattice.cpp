@@ -3,10 +3,12 @@
 //   HNF (Prop. 1): column operations A C = (H | 0), C unimodular, in checked __int128.
 //   B = C[:, m:]            (Thm. 1 setup: Ker_Z(A) = L(B)).
 //   LLL (Alg. 1) with the paper's Siegel test ||B*_{k-1}||^2 > 2 ||B*_k||^2 (Def. P:136-144):
-//     integer basis updates are exact (checked); the Gram-Schmidt data are long double, recomputed from
-//     exact inner products at every visit of k (Schnorr-Euchner style).
+//     integer basis updates are exact; the Gram-Schmidt data are recomputed from exact inner products at
+//     every visit of k (Schnorr-Euchner style). Fast path: basis in doubles while |entries| < 2^20 (exact
+//     integers and inner products), fp64 Gram-Schmidt; otherwise checked __int128 + long double.
 //   B+ = (B^T B)^{-1} B^T (Remark P:321-324): exact Gram matrix, fp64 Cholesky solve.
 // Independent of oracle/lattice.py (which uses Python big integers and a different LLL bookkeeping).
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -106,8 +108,113 @@ int host_kernel_basis(const int32_t* A, int m, int n, std::vector<int64_t>& B, s
     return 0;
 }
 
+namespace {
+
+// 4 independent accumulators (ILP / vectorisation); the sum of exact integer products is exact in double
+// while every partial sum stays below 2^53 (guaranteed by the caller's entry bound)
+inline double dot4(const double* a, const double* b, int len) {
+    double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    int r = 0;
+    for (; r + 4 <= len; r += 4) {
+        s0 += a[r] * b[r];
+        s1 += a[r + 1] * b[r + 1];
+        s2 += a[r + 2] * b[r + 2];
+        s3 += a[r + 3] * b[r + 3];
+    }
+    for (; r < len; ++r) s0 += a[r] * b[r];
+    return (s0 + s1) + (s2 + s3);
+}
+
+// LLL fast path: the same algorithm as the exact path below (size reduction against j = k-1..0, Siegel test,
+// Schnorr-Euchner recomputation of row k), with the basis held in doubles. Valid while every entry stays below
+// 2^20 in magnitude: then every inner product is an exact integer (n * 2^40 < 2^53 for n <= 8192) and every
+// basis update is exact. Returns 0 on success, 1 if the bound would be exceeded (the caller then runs the exact
+// path from the original input), -3 on dependent columns.
+int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
+    constexpr double kMax = 1048576.0;   // 2^20
+    if (n > 8192) return 1;
+    std::vector<double> b((size_t)d * n);   // column k contiguous
+    for (int r = 0; r < n; ++r)
+        for (int k = 0; k < d; ++k) {
+            const int64_t v = Bnd[(size_t)r * d + k];
+            if (v >= (int64_t)kMax || v <= -(int64_t)kMax) return 1;
+            b[(size_t)k * n + r] = (double)v;
+        }
+    std::vector<double> mu((size_t)d * d, 0.0), rr((size_t)d * d, 0.0), Bs(d, 0.0);
+    auto col = [&](int k) { return &b[(size_t)k * n]; };
+    auto gso_row = [&](int k) {
+        double* rk = &rr[(size_t)k * d];
+        double* mk = &mu[(size_t)k * d];
+        for (int j = 0; j < k; ++j) {
+            const double s = dot4(col(k), col(j), n) - dot4(&mu[(size_t)j * d], rk, j);
+            rk[j] = s;
+            mk[j] = s / Bs[j];
+        }
+        Bs[k] = dot4(col(k), col(k), n) - dot4(mk, rk, k);
+    };
+    gso_row(0);
+    if (Bs[0] <= 0) {
+        err = "dependent kernel columns";
+        return -3;
+    }
+    int k = 1;
+    long iters = 0;
+    while (k < d) {
+        if (++iters > 200000000L) return 1;
+        for (int pass = 0; pass < 64; ++pass) {
+            gso_row(k);
+            bool changed = false;
+            for (int j = k - 1; j >= 0; --j) {
+                const double mkj = mu[(size_t)k * d + j];
+                const double q = std::nearbyint(mkj);
+                if (std::fabs(mkj) > 0.5 + 1e-12 && q != 0) {
+                    if (std::fabs(q) >= kMax) return 1;
+                    double* bk = col(k);
+                    const double* bj = col(j);
+                    double mx = 0;
+                    for (int r = 0; r < n; ++r) {
+                        bk[r] -= q * bj[r];   // exact: |q|, |b| < 2^20 -> |q b| < 2^40
+                        mx = std::fmax(mx, std::fabs(bk[r]));
+                    }
+                    if (mx >= kMax) return 1;
+                    for (int l = 0; l < j; ++l) mu[(size_t)k * d + l] -= q * mu[(size_t)j * d + l];
+                    mu[(size_t)k * d + j] -= q;
+                    changed = true;
+                }
+            }
+            if (!changed) break;
+        }
+        if (Bs[k] <= 0) {
+            err = "dependent kernel columns";
+            return -3;
+        }
+        if (Bs[k - 1] > 2.0 * Bs[k] * (1.0 + 1e-12)) {  // Siegel test (Alg. 1 line 5)
+            std::swap_ranges(col(k), col(k) + n, col(k - 1));
+            gso_row(k - 1);
+            k = (k - 1 > 1) ? k - 1 : 1;
+            if (k == 1) gso_row(0);
+        } else {
+            ++k;
+        }
+    }
+    for (int r = 0; r < n; ++r)
+        for (int kk = 0; kk < d; ++kk) Bnd[(size_t)r * d + kk] = (int64_t)b[(size_t)kk * n + r];
+    return 0;
+}
+
+}  // namespace
+
 int host_lll(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
     if (d <= 1) return 0;
+    {
+        std::vector<int64_t> trial = Bnd;
+        const int rc = lll_fast(trial, n, d, err);
+        if (rc <= 0) {
+            if (rc == 0) Bnd.swap(trial);
+            return rc;
+        }
+    }
+    // exact path (entries beyond the fast path's bound)
     // columns b_k as contiguous vectors
     std::vector<std::vector<i128>> b(d, std::vector<i128>(n));
     for (int r = 0; r < n; ++r)
@@ -189,8 +296,76 @@ int host_lll(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
     return 0;
 }
 
+namespace {
+
+// B+ fast path (|entries| < 2^20, n <= 8192): G = B^T B exactly in int64 from the rows' outer products (the
+// rows of a reduced kernel basis are sparse), fp64 Cholesky G = L L^T, G^{-1} = L^{-T} L^{-1}, then each column
+// of B+ = G^{-1} (row c of B) touches only the row's nonzeros. Returns 1 when out of range (exact path instead).
+int pinv_fast(const std::vector<int64_t>& B, int n, int d, std::vector<double>& Bp, std::string& err) {
+    if (n > 8192) return 1;
+    std::vector<std::vector<std::pair<int, int64_t>>> rows(n);
+    for (int r = 0; r < n; ++r)
+        for (int j = 0; j < d; ++j) {
+            const int64_t v = B[(size_t)r * d + j];
+            if (v >= (1 << 20) || v <= -(1 << 20)) return 1;
+            if (v) rows[r].emplace_back(j, v);
+        }
+    std::vector<int64_t> Gi((size_t)d * d, 0);   // |G_ij| <= n 2^40 < 2^53: exact, and exact as a double
+    for (const auto& rw : rows)
+        for (const auto& a : rw)
+            for (const auto& b : rw)
+                if (b.first <= a.first) Gi[(size_t)a.first * d + b.first] += a.second * b.second;
+    std::vector<double> L((size_t)d * d, 0.0);   // lower triangle, row-major
+    for (int j = 0; j < d; ++j) {
+        double* Lj = &L[(size_t)j * d];
+        const double s = (double)Gi[(size_t)j * d + j] - dot4(Lj, Lj, j);
+        if (!(s > 0)) {
+            err = "B^T B is not positive definite";
+            return -3;
+        }
+        Lj[j] = std::sqrt(s);
+        const double inv = 1.0 / Lj[j];
+        for (int i = j + 1; i < d; ++i) {
+            double* Li = &L[(size_t)i * d];
+            Li[j] = ((double)Gi[(size_t)i * d + j] - dot4(Li, Lj, j)) * inv;
+        }
+    }
+    // X = L^{-1} (lower triangular), stored transposed (Xt[j][i] = X[i][j]) so both loops below read rows
+    std::vector<double> Xt((size_t)d * d, 0.0), col(d);
+    for (int j = 0; j < d; ++j) {   // column j of X: L x = e_j, x_i = 0 for i < j
+        for (int i = 0; i < d; ++i) col[i] = 0.0;
+        col[j] = 1.0 / L[(size_t)j * d + j];
+        for (int i = j + 1; i < d; ++i) {
+            const double* Li = &L[(size_t)i * d];
+            col[i] = -dot4(Li + j, &col[j], i - j) / Li[i];
+        }
+        for (int i = j; i < d; ++i) Xt[(size_t)j * d + i] = col[i];
+    }
+    // G^{-1} = X^T X: (G^{-1})_{ab} = sum_{i >= max(a,b)} X_ia X_ib = dot of Xt rows a and b from max(a, b)
+    std::vector<double> Ginv((size_t)d * d);
+    for (int a = 0; a < d; ++a)
+        for (int b = 0; b <= a; ++b) {
+            const double v = dot4(&Xt[(size_t)a * d + a], &Xt[(size_t)b * d + a], d - a);
+            Ginv[(size_t)a * d + b] = Ginv[(size_t)b * d + a] = v;
+        }
+    Bp.assign((size_t)d * n, 0.0);
+    for (int c = 0; c < n; ++c)
+        for (const auto& e : rows[c]) {
+            const double v = (double)e.second;
+            const double* g = &Ginv[(size_t)e.first * d];   // column e.first of the symmetric G^{-1}
+            for (int i = 0; i < d; ++i) Bp[(size_t)i * n + c] += v * g[i];
+        }
+    return 0;
+}
+
+}  // namespace
+
 int host_pinv(const std::vector<int64_t>& B, int n, int d, std::vector<double>& Bp, std::string& err) {
-    // G = B^T B exactly, then Cholesky G = L L^T in long double, Bp = G^{-1} B^T.
+    {
+        const int rc = pinv_fast(B, n, d, Bp, err);
+        if (rc <= 0) return rc;
+    }
+    // exact-Gram path: G = B^T B in __int128, then Cholesky G = L L^T in long double, Bp = G^{-1} B^T.
     typedef long double ld;
     std::vector<ld> G(size_t(d) * d);
     for (int i = 0; i < d; ++i)
