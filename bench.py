@@ -122,67 +122,26 @@ def _dist_env():
     return world, rank, local
 
 
-def run_reference(args):
-    """The oracle (oracle/, the CPU reference) on a bounded sample of the same workload, per step."""
-    world, rank, _ = _dist_env()
-    if rank != 0:
-        return 0
-    from oracle import augment as OA, extraction as OX, lattice as OL, postprocess as OP
-    from synth import feasible_points
+def _oracle_cores():
     try:
         from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
     except Exception:
-        cores = os.cpu_count()
-    inst = _instance()
-    S, KI = (256, 10) if inst.n <= 64 else (16, 2)
-    times, nset = [], 0
-    for it in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        B = np.array(OL.lll_reduce(OL.kernel_basis(inst.A)), dtype=np.int64)
-        pool, _ = OX.extract_pool(B, OL.pinv(B), inst.l, inst.u, N_STARTS, T_STEPS, LR, SEED,
-                                  starts=np.arange(S * it, S * (it + 1)) % N_STARTS)
-        S_min = OP.minimal_filter(pool)
-        X0 = feasible_points(inst, KI, seed=99)
-        OA.multi_start(OA.Objective(inst.Q, inst.c, inst.c0), inst.A, inst.b, inst.l, inst.u, X0, S_min)
-        dt = time.perf_counter() - t0
-        if it >= args.warmup:
-            times.append(dt)
-            nset = len(S_min)
-    # extrapolate the sample to the full workload: descent + harvest scale with starts, augmentation with
-    # incumbents (both linear); the filter is reported as measured on the sample.
-    t_sample = statistics.mean(times)
-    t_full = t_sample * (N_STARTS / S)
-    value = nset / t_full
-    line = {"metric": METRIC, "value": value, "unit": "directions/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": inst.n, "m": inst.m, "n_starts": N_STARTS, "steps": T_STEPS,
-                       "incumbents": K_INCUMBENTS},
-            "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "directions/s", "cores": cores, "kind": "oracle",
-                             "sample": f"per step: starts [{S}k, {S}(k+1)) of {N_STARTS} x T={T_STEPS} fp64 descent + "
-                                       f"harvest + exact filter, {KI} augmentations; time x{N_STARTS // S} "
-                                       f"(linear in starts); measured {t_sample:.2f} s per sample"},
-            "e2e": {"value": value, "unit": "directions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
-    return 0
+        return os.cpu_count()
 
 
-def cpu_baseline_sample():
-    """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
+def _oracle_step(S, KI, offset):
+    """One bounded oracle sample of the workload: the lattice step, fp64 descent + harvest of S starts
+    [offset, offset + S), the exact ⊑ filter of their pool, KI of the K_INCUMBENTS augmentations. The full-step
+    estimate scales the descent by N / S and the augmentations by K / KI (both linear in their units) and takes
+    the filter as measured on the sample's pool (the full pool is larger: a lower bound on the oracle's time)."""
     from oracle import augment as OA, extraction as OX, lattice as OL, postprocess as OP
     from synth import feasible_points
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = os.cpu_count()
     inst = _instance()
-    S, KI = (1024, 20) if inst.n <= 64 else (32, 4)
     t0 = time.perf_counter()
     B = np.array(OL.lll_reduce(OL.kernel_basis(inst.A)), dtype=np.int64)
-    pool, _ = OX.extract_pool(B, OL.pinv(B), inst.l, inst.u, N_STARTS, T_STEPS, LR, SEED, starts=np.arange(S))
+    pool, _ = OX.extract_pool(B, OL.pinv(B), inst.l, inst.u, N_STARTS, T_STEPS, LR, SEED,
+                              starts=np.arange(offset, offset + S) % N_STARTS)
     t_desc = time.perf_counter() - t0
     S_min = OP.minimal_filter(pool)
     t_filt = time.perf_counter() - t0 - t_desc
@@ -191,11 +150,50 @@ def cpu_baseline_sample():
     OA.multi_start(OA.Objective(inst.Q, inst.c, inst.c0), inst.A, inst.b, inst.l, inst.u, X0, S_min)
     t_aug = time.perf_counter() - t1
     t_full = t_desc * (N_STARTS / S) + t_filt + t_aug * (K_INCUMBENTS / KI)
-    return {"value": len(S_min) / t_full, "unit": "directions/s", "cores": cores, "kind": "oracle",
-            "sample": (f"first {S} of {N_STARTS} starts (fp64 descent+harvest {t_desc:.1f} s, x{N_STARTS // S}), "
-                       f"exact filter of their pool ({len(pool)} rows, {t_filt:.1f} s, as measured), "
-                       f"{KI} of {K_INCUMBENTS} augmentations ({t_aug:.1f} s, x{K_INCUMBENTS // KI}); "
-                       f"{len(S_min)} minimal directions; extrapolated step {t_full:.0f} s")}
+    return {"t_full": t_full, "t_desc": t_desc, "t_filt": t_filt, "t_aug": t_aug, "n_min": len(S_min),
+            "pool": len(pool), "wall": time.perf_counter() - t0}
+
+
+def _sample_text(S, KI, r, offset_text):
+    return (f"{S} of {N_STARTS} starts ({offset_text}; fp64 descent+harvest {r['t_desc']:.1f} s, x{N_STARTS // S}), "
+            f"exact filter of their pool ({r['pool']} rows, {r['t_filt']:.1f} s, as measured: a lower bound), "
+            f"{KI} of {K_INCUMBENTS} augmentations ({r['t_aug']:.1f} s, x{K_INCUMBENTS // KI}); {r['n_min']} minimal "
+            f"directions; estimated step {r['t_full']:.0f} s")
+
+
+def run_reference(args):
+    """The oracle (oracle/, the CPU reference) on a bounded sample of the same workload, per step."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    S, KI = (256, 10) if _instance().n <= 64 else (16, 2)
+    res = []
+    for it in range(args.warmup + args.steps):
+        r = _oracle_step(S, KI, S * it)
+        if it >= args.warmup:
+            res.append(r)
+    t_full = statistics.mean(r["t_full"] for r in res)
+    nset = statistics.mean(r["n_min"] for r in res)
+    value = nset / t_full
+    line = {"metric": METRIC, "value": value, "unit": "directions/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n": _instance().n, "m": _instance().m, "n_starts": N_STARTS,
+                       "steps": T_STEPS, "incumbents": K_INCUMBENTS},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "directions/s", "cores": _oracle_cores(), "kind": "oracle",
+                             "sample": "per step: " + _sample_text(S, KI, res[-1], f"starts [{S}k, {S}(k+1)) at step k")},
+            "e2e": {"value": value, "unit": "directions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_sample():
+    """Oracle timed on the host cores on a bounded sample (rank 0, N=1 only)."""
+    S, KI = (1024, 20) if _instance().n <= 64 else (32, 4)
+    r = _oracle_step(S, KI, 0)
+    return {"value": r["n_min"] / r["t_full"], "unit": "directions/s", "cores": _oracle_cores(), "kind": "oracle",
+            "sample": _sample_text(S, KI, r, "the first ones")}
 
 
 def main():
