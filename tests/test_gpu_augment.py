@@ -89,3 +89,39 @@ def test_augment_many_matches_single(gpu_lib):
         f = OA.Objective(Qs[t], cs[t])
         xo, fo, _ = OA.multi_start(f, base.A, bs[t], base.l, base.u, X0s[t], S)
         assert xb[t].tolist() == xo.tolist() and abs(fb[t] - fo) <= 1e-9 * max(1, abs(fo))
+
+
+def test_c4_full_batch_properties(gpu_lib):
+    """configs[3] at full size: 1,000 (f, b) instances x 256 incumbents against one C2a extraction (65,536
+    starts). Properties that hold at any size, checked exactly on the host for every instance: x_best is
+    feasible, f_best = f(x_best), no incumbent is better, and x_best is a local optimum of Alg. 2 (no g in
+    S ∪ -S with a feasible step λ >= 1 improves f). Sampled instances equal the single-instance call."""
+    from synth import c4_batch
+    base, insts = c4_batch()
+    ctx = gpu_lib.Context(base.A, base.l, base.u)
+    ds = ctx.extract(base.n_starts, base.steps, base.lr, base.seed)
+    S = ds.rows().astype(np.int64)
+    D = np.concatenate([S, -S])
+    Qs, cs, bs, X0s = zip(*insts)
+    xb, fb = ctx.augment_many(ds, Qs, cs, [0.0] * len(insts), bs, np.stack(X0s))
+    l, u = base.l.astype(np.int64), base.u.astype(np.int64)
+    for t, (Q, c, b, X0) in enumerate(insts):
+        Qi, ci = np.asarray(Q, np.int64), np.asarray(c, np.int64)
+        x = xb[t].astype(np.int64)
+        assert np.all(base.A @ x == b) and np.all(x >= l) and np.all(x <= u)
+        two_f = int(x @ Qi @ x + 2 * ci @ x)
+        assert fb[t] == two_f / 2
+        X = np.asarray(X0, np.int64)
+        assert two_f <= int(np.min(np.einsum("ki,ij,kj->k", X, Qi, X) + 2 * X @ ci))
+        # local optimality: 2Δ(λ) = 2λ gᵀ(Qx + c) + λ² gᵀQg >= 0 for every g in D and feasible λ >= 1
+        with np.errstate(divide="ignore"):
+            up = np.where(D > 0, (u - x)[None, :] // np.where(D > 0, D, 1), np.iinfo(np.int64).max)
+            dn = np.where(D < 0, (x - l)[None, :] // np.where(D < 0, -D, 1), np.iinfo(np.int64).max)
+        lam_max = np.minimum(up.min(axis=1), dn.min(axis=1))
+        lin, quad = D @ (Qi @ x + ci), np.einsum("ki,ij,kj->k", D, Qi, D)
+        for lam in range(1, int(lam_max.max(initial=0)) + 1):
+            ok = lam <= lam_max
+            assert np.all(2 * lam * lin[ok] + lam * lam * quad[ok] >= 0), (t, lam)
+    for t in (0, 499, 999):
+        x1, f1, _, _ = ctx.augment(ds, Qs[t], cs[t], 0.0, bs[t], X0s[t])
+        assert xb[t].tolist() == x1.tolist() and fb[t] == f1
