@@ -101,12 +101,12 @@ struct maple_dirset {
     int32_t* D_nnz = nullptr;     // ELL of D (lazily built)
     int16_t* D_col = nullptr;
     int8_t* D_val = nullptr;
-    int D_nzmax = 0;
+    int D_nzmax = 1;   // ELL width of D: bound on the rows' nonzero counts, known when the set is finished
     cudaEvent_t ready = nullptr;  // recorded after the last device write to this set
 };
 
 // counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
-enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_N = 6 };
+enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_NZMAX = 6, C_N = 7 };
 
 #define FAIL(code, msg)              \
     do {                             \
@@ -208,7 +208,7 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     CU(launch_filter(dpool, K, ctx->flags.as<uint8_t>(), fw, filter_minimal, s, &nl));
     ctx->launches += nl;
     CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), dpool, K, np, ctx->tmp_rows.as<int8_t>(),
-                      counters(ctx) + C_KEEP, s));
+                      counters(ctx) + C_KEEP, counters(ctx) + C_NZMAX, s));
     ctx->launches++;
     CU(cudaEventRecord(ctx->ev[4], s));
     unsigned long long h[C_N];
@@ -227,6 +227,7 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     ds->size = M;
     ds->pool_size = (int64_t)h[C_POOL] - (int64_t)h[C_BAD];
     ds->n_bad = (int64_t)h[C_BAD];
+    ds->D_nzmax = std::max(1, (int)h[C_NZMAX]);   // the most nonzeros of a row of the set (compact kernel)
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ds->rows), std::max<int64_t>(M, 1) * np, s);
     if (e != cudaSuccess) {
         delete ds;
@@ -872,28 +873,17 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     maple_dirset* dsm = const_cast<maple_dirset*>(ds);
     const int64_t K = ds->size;
     if (!dsm->D && K > 0) {
-        DevBuf un;
-        CU(un.ensure((size_t)2 * K * np));
-        CU(launch_signed_union(ds->rows, K, np, un.as<int8_t>(), s));
-        ctx->launches++;
+        // D = S ∪ -S in lexicographic order (the tie-break order of Alg. 2, reading #17) by a merge of the sorted
+        // set with its reversed negation, then its ELL form; stream-ordered, no host synchronisation
         CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D), (size_t)2 * K * np, s));
-        CU(ctx->sortkeys.ensure((size_t)2 * K * np));
-        CU(ctx->sidx0.ensure((size_t)2 * K * 4));
-        CU(ctx->sidx1.ensure((size_t)2 * K * 4));
-        int nl = 0;
-        CU(launch_lex_sort(un.as<int8_t>(), 2 * K, n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
-                           ctx->sidx1.as<int32_t>(), dsm->D, s, &nl));
-        ctx->launches += nl;
-        CU(cudaStreamSynchronize(s));
-        un.release();
+        CU(launch_signed_merge(ds->rows, K, n, np, dsm->D, s));
+        ctx->launches++;
+        const int w = dsm->D_nzmax;
         CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_nnz), (size_t)2 * K * sizeof(int32_t), s));
-        DevBuf nzd;
-        CU(nzd.ensure(sizeof(int)));
-        CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, dsm->D_nnz, nzd.as<int>(), &dsm->D_col, &dsm->D_val,
-                              &dsm->D_nzmax, s));
-        ctx->launches += 2;
-        CU(cudaStreamSynchronize(s));
-        nzd.release();
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_col), (size_t)2 * K * w * sizeof(int16_t), s));
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_val), (size_t)2 * K * w, s));
+        CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, w, dsm->D_nnz, dsm->D_col, dsm->D_val, s));
+        ctx->launches++;
     }
     // objective data (dense Q per instance)
     std::vector<double> Q((size_t)n_inst * n * n, 0.0), c((size_t)n_inst * n), c0(n_inst);

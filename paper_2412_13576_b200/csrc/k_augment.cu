@@ -23,28 +23,20 @@ namespace {
 constexpr int kAugThreads = 256;
 constexpr int kMaxN = 1024;
 
-// ELL of D: for each row e, nnz[e] <= nzmax columns (ascending) and values
-__global__ void ell_count_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax) {
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nD; e += gridDim.x * blockDim.x) {
-        const int8_t* g = dirs + (size_t)e * n_pad;
-        int c = 0;
-        for (int i = 0; i < n; ++i) c += g[i] != 0;
-        nnz[e] = c;
-        atomicMax(nzmax, c);
-    }
-}
-
-__global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int nzmax, int16_t* col,
-                                int8_t* val) {
+// ELL of D: for each row e, its nnz[e] (<= width, the check kernel's bound over the set) columns in ascending
+// order and their values
+__global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int width, int16_t* col,
+                                int8_t* val, int32_t* nnz) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nD; e += gridDim.x * blockDim.x) {
         const int8_t* g = dirs + (size_t)e * n_pad;
         int c = 0;
         for (int i = 0; i < n; ++i)
-            if (g[i]) {
-                col[(size_t)e * nzmax + c] = (int16_t)i;
-                val[(size_t)e * nzmax + c] = g[i];
+            if (g[i] && c < width) {
+                col[(size_t)e * width + c] = (int16_t)i;
+                val[(size_t)e * width + c] = g[i];
                 ++c;
             }
+        nnz[e] = c;
     }
 }
 
@@ -245,24 +237,11 @@ __global__ void best_kernel(AugmentParams p, int32_t* xbest, double* f2best, int
 
 }  // namespace
 
-cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax_dev,
-                               int16_t** col, int8_t** val, int* nzmax_host, cudaStream_t s) {
-    if (nD <= 0) {
-        *nzmax_host = 0;
-        return cudaSuccess;
-    }
-    cudaError_t e = cudaMemsetAsync(nzmax_dev, 0, sizeof(int), s);
-    if (e != cudaSuccess) return e;
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, int16_t* col,
+                               int8_t* val, cudaStream_t s) {
+    if (nD <= 0) return cudaSuccess;
     const unsigned blocks = (unsigned)std::min(148 * 8, (nD + 255) / 256);
-    ell_count_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, nnz, nzmax_dev);
-    if ((e = cudaMemcpyAsync(nzmax_host, nzmax_dev, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
-    const int nz = std::max(*nzmax_host, 1);
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(col), (size_t)nD * nz * sizeof(int16_t), s)) != cudaSuccess)
-        return e;
-    if ((e = cudaMallocAsync(reinterpret_cast<void**>(val), (size_t)nD * nz, s)) != cudaSuccess) return e;
-    ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, nz, *col, *val);
-    *nzmax_host = nz;
+    ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, width, col, val, nnz);
     return cudaGetLastError();
 }
 
@@ -270,7 +249,7 @@ cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* 
     if (p.n_inst <= 0 || p.k0 <= 0) return cudaSuccess;
     const size_t smem = (size_t)p.k0 * ((size_t)p.n * 4 + 8);
     const int staged = smem <= 160 * 1024;
-    if (staged && smem > 48 * 1024) {
+    if (staged) {
         cudaError_t e = cudaFuncSetAttribute(best_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
@@ -294,7 +273,7 @@ cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s) {
     const size_t nD2 = (size_t)2 * p.n_dir;
     const size_t smem = nD2 * 8 + nD2 * 4 + nD2 * p.nzmax * 3 + 16;
     const int staged = smem <= 96 * 1024;
-    if (staged && smem > 48 * 1024) {
+    if (staged) {   // dynamic + ~12 KB static may pass the 48 KB default even when the dynamic part does not
         cudaError_t e = cudaFuncSetAttribute(augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }

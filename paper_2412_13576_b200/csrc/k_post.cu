@@ -361,17 +361,30 @@ __global__ void clear_keep_kernel(const unsigned long long* dcount, int64_t cap,
         keep[r] = 0;
 }
 
+// Gather the selected rows; *nz_max gets the largest nonzero count among them (the ELL width of the set, known
+// to the host at the extraction's one synchronisation, so augmentation needs none).
 __global__ void compact_kernel(const int8_t* __restrict__ rows, const uint8_t* sel, const unsigned long long* dcount,
-                               int64_t cap, int n_pad, int8_t* out, unsigned long long* n_out) {
+                               int64_t cap, int n_pad, int8_t* out, unsigned long long* n_out,
+                               unsigned long long* nz_max) {
     const int nw = n_pad / 16;
     const int64_t count = dev_count(dcount, cap);
+    int my_nz = 0;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
         if (!sel[r]) continue;
         const unsigned long long o = atomicAdd(n_out, 1ULL);
         const int4* s = reinterpret_cast<const int4*>(rows + (size_t)r * n_pad);
         int4* dd = reinterpret_cast<int4*>(out + (size_t)o * n_pad);
-        for (int i = 0; i < nw; ++i) dd[i] = s[i];
+        int nz = 0;
+        for (int i = 0; i < nw; ++i) {
+            const int4 v = s[i];
+            dd[i] = v;
+            nz += (__popc(__vcmpne4((uint32_t)v.x, 0u)) + __popc(__vcmpne4((uint32_t)v.y, 0u)) +
+                   __popc(__vcmpne4((uint32_t)v.z, 0u)) + __popc(__vcmpne4((uint32_t)v.w, 0u))) >> 3;
+        }
+        my_nz = max(my_nz, nz);
     }
+    my_nz = __reduce_max_sync(0xffffffffu, my_nz);
+    if ((threadIdx.x & 31) == 0 && my_nz) atomicMax(nz_max, (unsigned long long)my_nz);
 }
 
 __global__ void sortkey_kernel(const int8_t* __restrict__ rows, int64_t k, int n_pad, uint32_t* keys, int32_t* idx) {
@@ -489,11 +502,35 @@ __global__ void gather_kernel(const int8_t* __restrict__ rows, const int32_t* id
     }
 }
 
-__global__ void signed_union_kernel(const int8_t* __restrict__ rows, int64_t k, int n_pad, int8_t* out) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < k * n_pad; t += (int64_t)gridDim.x * blockDim.x) {
-        const int8_t v = rows[t];
-        out[t] = v;
-        out[k * n_pad + t] = (int8_t)(-v);
+// lexicographic compare of row a with (neg ? -b : b), int8 entries, first n coordinates
+__device__ __forceinline__ int lex_cmp_signed(const int8_t* a, const int8_t* b, bool neg, int n) {
+    for (int k = 0; k < n; ++k) {
+        const int x = a[k], y = neg ? -(int)b[k] : (int)b[k];
+        if (x != y) return x < y ? -1 : 1;
+    }
+    return 0;
+}
+
+// D = S ∪ -S in lexicographic order, from S sorted ascending: negation reverses the order, so -S ascending is
+// N[j] = -S[k-1-j], and no row of S equals a row of -S (canonical rows have a positive first nonzero). Each row
+// goes to its own index plus its rank in the other sequence (binary search): a merge, no sort.
+__global__ void signed_merge_kernel(const int8_t* __restrict__ S, int64_t k, int n, int n_pad, int8_t* out) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * k; t += (int64_t)gridDim.x * blockDim.x) {
+        const bool from_neg = t >= k;
+        const int64_t i = from_neg ? t - k : t;                 // index within its own ascending sequence
+        const int8_t* self = from_neg ? S + (size_t)(k - 1 - i) * n_pad : S + (size_t)i * n_pad;
+        // rank: number of rows of the other sequence that are smaller than this row (as signed rows)
+        int64_t lo = 0, hi = k;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            // c = cmp(other[mid], this row)
+            const int c = from_neg ? lex_cmp_signed(S + (size_t)mid * n_pad, self, true, n)          // S[mid] vs -self
+                                   : -lex_cmp_signed(self, S + (size_t)(k - 1 - mid) * n_pad, true, n);  // N[mid] vs self
+            if (c < 0) lo = mid + 1;
+            else hi = mid;
+        }
+        int8_t* dst = out + (size_t)(i + lo) * n_pad;
+        for (int q = 0; q < n_pad; ++q) dst[q] = from_neg ? (int8_t)(-self[q]) : self[q];
     }
 }
 
@@ -558,16 +595,16 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
     return cudaGetLastError();
 }
 
-cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t* out, cudaStream_t s) {
+cudaError_t launch_signed_merge(const int8_t* S, int64_t k, int n, int n_pad, int8_t* out, cudaStream_t s) {
     if (k <= 0) return cudaSuccess;
-    signed_union_kernel<<<grid_for(k * n_pad), 256, 0, s>>>(rows, k, n_pad, out);
+    signed_merge_kernel<<<grid_for(2 * k), 256, 0, s>>>(S, k, n, n_pad, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, const unsigned long long* dcount, int64_t cap,
-                           int n_pad, int8_t* out, unsigned long long* n_out, cudaStream_t s) {
+                           int n_pad, int8_t* out, unsigned long long* n_out, unsigned long long* nz_max, cudaStream_t s) {
     if (cap <= 0) return cudaSuccess;
-    compact_kernel<<<grid_for(cap), 256, 0, s>>>(rows, sel, dcount, cap, n_pad, out, n_out);
+    compact_kernel<<<grid_for(cap), 256, 0, s>>>(rows, sel, dcount, cap, n_pad, out, n_out, nz_max);
     return cudaGetLastError();
 }
 

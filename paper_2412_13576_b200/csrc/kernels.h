@@ -101,9 +101,10 @@ cudaError_t launch_check_codes(const int8_t* rows, const unsigned long long* dco
 // keep[r] (and witness[r]) for the ⊑ filter, or keep = valid when filter_minimal == 0
 cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const uint8_t* valid, FilterWork& fw,
                           int filter_minimal, cudaStream_t s, int* launches);
-// Gather rows with sel[r] != 0 into out (stride n_pad) in an arbitrary order; count to *n_out (device).
+// Gather rows with sel[r] != 0 into out (stride n_pad) in an arbitrary order; count to *n_out (device), the
+// largest nonzero count among them to *nz_max (atomic max).
 cudaError_t launch_compact(const int8_t* rows, const uint8_t* sel, const unsigned long long* dcount, int64_t cap,
-                           int n_pad, int8_t* out, unsigned long long* n_out, cudaStream_t s);
+                           int n_pad, int8_t* out, unsigned long long* n_out, unsigned long long* nz_max, cudaStream_t s);
 // Lexicographic sort of k rows (stride n_pad, n bytes compared as signed int8). keys/idx scratch:
 // keys: k * n_pad/4 uint32, idx0/idx1: k int32. Result written to out rows.
 cudaError_t launch_lex_sort(const int8_t* rows, int64_t k, int n, int n_pad, uint32_t* keys, int32_t* idx0,
@@ -155,11 +156,11 @@ struct AugmentParams {
 };
 cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s);
 cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s);
-// ELL form of the 2K rows of D (allocates *col, *val with cudaMalloc; *nzmax_host receives the width)
-cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int32_t* nnz, int* nzmax_dev,
-                               int16_t** col, int8_t** val, int* nzmax_host, cudaStream_t s);
+// ELL form of the 2K rows of D into col / val (nD x width, width >= every row's nonzero count) and nnz
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, int16_t* col,
+                               int8_t* val, cudaStream_t s);
 cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s);
-// D = rows ∪ -rows (2k rows, stride n_pad) written to out (unsorted; the caller lex-sorts it)
-cudaError_t launch_signed_union(const int8_t* rows, int64_t k, int n_pad, int8_t* out, cudaStream_t s);
+// D = S ∪ -S in lexicographic order from a lexicographically sorted canonical S (a merge; 2k rows into out)
+cudaError_t launch_signed_merge(const int8_t* S, int64_t k, int n, int n_pad, int8_t* out, cudaStream_t s);
 
 }  // namespace maple
