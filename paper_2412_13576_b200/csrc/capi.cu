@@ -46,6 +46,37 @@ struct DevBuf {
     T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// Pinned host staging for per-call uploads: a copy from pageable memory first synchronises the stream, a copy
+// from pinned memory is asynchronous. Bump-allocated per call; every call that uses it synchronises on the
+// context stream before returning, so the next call may reuse it.
+struct HostStage {
+    unsigned char* p = nullptr;
+    size_t bytes = 0, used = 0;
+    cudaError_t reserve(size_t want) {
+        used = 0;
+        if (want <= bytes) return cudaSuccess;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        const size_t b = std::max<size_t>(want, 4096);
+        cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&p), b);
+        if (e == cudaSuccess) bytes = b;
+        return e;
+    }
+    template <class T>
+    T* take(size_t count) {   // 16-byte aligned slice; reserve() sized the total
+        used = (used + 15) & ~size_t(15);
+        T* r = reinterpret_cast<T*>(p + used);
+        used += count * sizeof(T);
+        return r;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = used = 0;
+    }
+};
+
 inline int round_up(int v, int a) { return (v + a - 1) / a * a; }
 inline uint64_t next_pow2(uint64_t v) {
     uint64_t p = 1;
@@ -64,6 +95,9 @@ struct maple_ctx {
     std::vector<double> Bp;       // d x n
     // device constants
     DevBuf A_rowptr, A_col, A_val, dl, du, dbox, B_nd, B_dn, B8, dBp, th_off, th_c0, th_c1;
+    HostStage stage_aug, stage_tab;   // pinned upload staging (augmentation inputs, Adam step table)
+    int tab_T = -1;                   // the step table on the device was built for (tab_T, tab_lr, betas)
+    double tab_lr = 0, tab_b1 = 0, tab_b2 = 0;
     DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned;   // SIMT schedules of B (sparse_ell.h)
     int ell_conflicts = 0;
     DevBuf AT_ptr, AT_row, AT_val, fb, frows, fX;
@@ -285,16 +319,23 @@ int insert_rows_and_finish(maple_ctx* ctx, const int8_t* drows, int64_t k, int s
 }
 
 int build_step_table(maple_ctx* ctx, int T, double lr) {
-    // per step t: (lr / (1 - beta1^t), sqrt(1 - beta2^t), 1 / sqrt(1 - beta2^t)) computed in fp64 (torch scalars)
-    std::vector<float4> tab(T);
+    // per step t: (lr / (1 - beta1^t), sqrt(1 - beta2^t), 1 / sqrt(1 - beta2^t)) computed in fp64 (torch scalars);
+    // rebuilt only when (T, lr, betas) change. The pinned upload is stream-ordered: the extraction's one
+    // synchronisation follows it, so the staging buffer is free again when the next call rebuilds.
+    if (T == ctx->tab_T && lr == ctx->tab_lr && ctx->beta1 == ctx->tab_b1 && ctx->beta2 == ctx->tab_b2) return MAPLE_OK;
+    CU(ctx->stage_tab.reserve(sizeof(float4) * T));
+    float4* tab = ctx->stage_tab.take<float4>(T);
     for (int t = 1; t <= T; ++t) {
         const double bc1 = 1.0 - std::pow(ctx->beta1, t);
         const double bc2s = std::sqrt(1.0 - std::pow(ctx->beta2, t));
         tab[t - 1] = make_float4((float)(lr / bc1), (float)bc2s, (float)(1.0 / bc2s), 0.f);
     }
     CU(ctx->step_tab.ensure(sizeof(float4) * T));
-    CU(cudaMemcpyAsync(ctx->step_tab.p, tab.data(), sizeof(float4) * T, cudaMemcpyHostToDevice, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpyAsync(ctx->step_tab.p, tab, sizeof(float4) * T, cudaMemcpyHostToDevice, ctx->stream));
+    ctx->tab_T = T;
+    ctx->tab_lr = lr;
+    ctx->tab_b1 = ctx->beta1;
+    ctx->tab_b2 = ctx->beta2;
     return MAPLE_OK;
 }
 
@@ -567,6 +608,8 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->af2b};
     for (DevBuf* b : bufs) b->release();
     cudaStreamSynchronize(ctx->stream);
+    ctx->stage_aug.release();
+    ctx->stage_tab.release();
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
@@ -885,10 +928,18 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
         CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, w, dsm->D_nnz, dsm->D_col, dsm->D_val, s));
         ctx->launches++;
     }
-    // objective data (dense Q per instance)
-    std::vector<double> Q((size_t)n_inst * n * n, 0.0), c((size_t)n_inst * n), c0(n_inst);
+    // objective data (dense Q per instance), staged in pinned memory
+    const int64_t ninc = (int64_t)n_inst * k0;
+    const size_t nQ = (size_t)n_inst * n * n, nc = (size_t)n_inst * n;
+    CU(ctx->stage_aug.reserve(nQ * 8 + nc * 8 + (size_t)n_inst * 8 + (size_t)ninc * n * 4 + 64));
+    double* Q = ctx->stage_aug.take<double>(nQ);
+    double* c = ctx->stage_aug.take<double>(nc);
+    double* c0 = ctx->stage_aug.take<double>(n_inst);
+    int32_t* X0 = ctx->stage_aug.take<int32_t>((size_t)ninc * n);
+    std::memset(Q, 0, nQ * 8);
+    std::memcpy(X0, x0, (size_t)ninc * n * 4);
     for (int t = 0; t < n_inst; ++t) {
-        double* Qt = Q.data() + (size_t)t * n * n;
+        double* Qt = Q + (size_t)t * n * n;
         if (f[t].kind == MAPLE_OBJ_QUADRATIC) {
             // the kernels use grad = Q x + c, which is the gradient of 1/2 x^T Q x only for symmetric Q:
             // use the symmetric part (same objective values, exact in fp64 for integer data)
@@ -897,23 +948,22 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
                     Qt[(size_t)i * n + j] = 0.5 * (f[t].Q[(size_t)i * n + j] + f[t].Q[(size_t)j * n + i]);
         } else
             for (int i = 0; i < n; ++i) Qt[(size_t)i * n + i] = f[t].Q[i];
-        std::memcpy(c.data() + (size_t)t * n, f[t].c, sizeof(double) * n);
+        std::memcpy(c + (size_t)t * n, f[t].c, sizeof(double) * n);
         c0[t] = f[t].c0;
     }
-    const int64_t ninc = (int64_t)n_inst * k0;
-    CU(ctx->aQ.ensure(Q.size() * 8));
-    CU(ctx->ac.ensure(c.size() * 8));
-    CU(ctx->ac0.ensure(c0.size() * 8));
+    CU(ctx->aQ.ensure(nQ * 8));
+    CU(ctx->ac.ensure(nc * 8));
+    CU(ctx->ac0.ensure((size_t)n_inst * 8));
     CU(ctx->aqg.ensure((size_t)std::max<int64_t>(2 * K, 1) * n_inst * 8));
     CU(ctx->aX.ensure((size_t)ninc * n * 4));
     CU(ctx->aF2.ensure((size_t)ninc * 8));
     CU(ctx->aIt.ensure((size_t)ninc * 4));
     CU(ctx->axb.ensure((size_t)n_inst * n * 4));
     CU(ctx->af2b.ensure((size_t)n_inst * 8));
-    CU(cudaMemcpyAsync(ctx->aQ.p, Q.data(), Q.size() * 8, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->ac.p, c.data(), c.size() * 8, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->ac0.p, c0.data(), c0.size() * 8, cudaMemcpyHostToDevice, s));
-    CU(cudaMemcpyAsync(ctx->aX.p, x0, (size_t)ninc * n * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->aQ.p, Q, nQ * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->ac.p, c, nc * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->ac0.p, c0, (size_t)n_inst * 8, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync(ctx->aX.p, X0, (size_t)ninc * n * 4, cudaMemcpyHostToDevice, s));
     AugmentParams p{};
     p.n = n;
     p.m = m;
