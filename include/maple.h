@@ -200,6 +200,11 @@ int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
 /* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05;
  * negative error code for a null context. Host only. */
 int maple_descent_kernel(const maple_ctx* ctx);
+/* Select the ⊑-minimality filter's pair enumeration (Def. 1-2; the kept set is the same for all):
+ * 0 = auto (indexed when n <= 1024), 1 = tiled (every row against all rows of smaller L1 norm), 2 = indexed
+ * (every row against the rows filed under one of its support coordinates with smaller L1 norm; needs n <= 1024).
+ * Returns BAD_ARG for a null context or another value. Host only. */
+int maple_set_filter_algorithm(maple_ctx* ctx, int32_t which);
 
 #ifdef __cplusplus
 }

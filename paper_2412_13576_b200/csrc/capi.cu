@@ -109,8 +109,10 @@ struct maple_ctx {
     double lam1 = 0.85, lam2 = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
     int filter_minimal = 1;
     int descent_kernel = 0;
+    int filter_algo = 0;          // 0 auto (indexed), 1 tiled, 2 indexed
     // workspace
-    DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, l1, hist, level_start, cursor, order, keep,
+    DevBuf ffreq, fkey, fbh, fbs, fbc, flrow, flsig;   // indexed filter (k_post.cu)
+    DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, sig, l1, hist, level_start, cursor, order, keep,
         witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
     DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b;
     int64_t cand_cap = 0, pool_cap = 0, want_cand = 0, want_pool = 0;
@@ -133,8 +135,7 @@ struct maple_dirset {
     int8_t* rows = nullptr;       // size x n_pad, canonical, lex sorted
     int8_t* D = nullptr;          // 2*size x n_pad: rows ∪ -rows, lex sorted (lazily built)
     int32_t* D_nnz = nullptr;     // ELL of D (lazily built)
-    int16_t* D_col = nullptr;
-    int8_t* D_val = nullptr;
+    uint32_t* D_words = nullptr;
     int D_nzmax = 1;   // ELL width of D: bound on the rows' nonzero counts, known when the set is finished
     cudaEvent_t ready = nullptr;  // recorded after the last device write to this set
 };
@@ -201,11 +202,22 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
         CU(ctx->order.ensure(K * 4));
         CU(ctx->l1.ensure(K * 4));
         CU(ctx->codes.ensure((size_t)K * 2 * std::max(ctx->Wh, 1) * 4));
+        CU(ctx->sig.ensure((size_t)K * 16));
+        CU(ctx->fkey.ensure((size_t)K * 4));
+        CU(ctx->flrow.ensure((size_t)K * 4));
+        CU(ctx->flsig.ensure((size_t)K * 16));
         CU(ctx->tmp_rows.ensure((size_t)K * np));
     }
     CU(ctx->hist.ensure((size_t)(ctx->Lh + 2) * 4));
     CU(ctx->level_start.ensure((size_t)(ctx->Lh + 2) * 4));
     CU(ctx->cursor.ensure((size_t)(ctx->Lh + 2) * 4));
+    {
+        const size_t nbins = (size_t)ctx->n * (ctx->Lh + 1);
+        CU(ctx->ffreq.ensure((size_t)ctx->n * 4));
+        CU(ctx->fbh.ensure(nbins * 4));
+        CU(ctx->fbs.ensure((nbins + 1) * 4));
+        CU(ctx->fbc.ensure(nbins * 4 + 4));   // + the undecided-row counter
+    }
     CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
     CU(cudaMemsetAsync(ctx->idx.p, 0xFF, ctx->table_slots * 4, ctx->stream));
     CU(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_N, ctx->stream));
@@ -232,7 +244,11 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->binary, ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
                   ctx->th_c1.as<int32_t>(), ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
-                  ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh};
+                  ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh, ctx->sig.as<uint4>(),
+                  ctx->filter_algo == 1 || ctx->n > 1024 ? 1 : 2, 0, ctx->pool.as<int8_t>(), ctx->ffreq.as<int32_t>(),
+                  ctx->fkey.as<int32_t>(), ctx->fbh.as<int32_t>(), ctx->fbs.as<int32_t>(), ctx->fbc.as<int32_t>(),
+                  ctx->flrow.as<int32_t>(), ctx->flsig.as<uint4>(),
+                  ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1)};
     const unsigned long long* dpool = counters(ctx) + C_POOL;
     CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, filter_minimal, ctx->flags.as<uint8_t>(),
                           counters(ctx) + C_BAD, s));
@@ -601,7 +617,7 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
                       &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
-                      &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->l1,
+                      &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->sig, &ctx->ffreq, &ctx->fkey, &ctx->fbh, &ctx->fbs, &ctx->fbc, &ctx->flrow, &ctx->flsig, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
                       &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,
@@ -660,6 +676,12 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
     if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
+    return MAPLE_OK;
+}
+
+int maple_set_filter_algorithm(maple_ctx* ctx, int32_t which) {
+    if (!ctx || which < 0 || which > 2) return MAPLE_ERR_BAD_ARG;
+    ctx->filter_algo = which;
     return MAPLE_OK;
 }
 
@@ -849,8 +871,7 @@ void maple_dirset_free(maple_dirset* ds) {
     if (ds->rows) cudaFreeAsync(ds->rows, 0);
     if (ds->D) cudaFreeAsync(ds->D, 0);
     if (ds->D_nnz) cudaFreeAsync(ds->D_nnz, 0);
-    if (ds->D_col) cudaFreeAsync(ds->D_col, 0);
-    if (ds->D_val) cudaFreeAsync(ds->D_val, 0);
+    if (ds->D_words) cudaFreeAsync(ds->D_words, 0);
     delete ds;
 }
 
@@ -923,9 +944,8 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
         ctx->launches++;
         const int w = dsm->D_nzmax;
         CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_nnz), (size_t)2 * K * sizeof(int32_t), s));
-        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_col), (size_t)2 * K * w * sizeof(int16_t), s));
-        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_val), (size_t)2 * K * w, s));
-        CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, w, dsm->D_nnz, dsm->D_col, dsm->D_val, s));
+        CU(cudaMallocAsync(reinterpret_cast<void**>(&dsm->D_words), (size_t)2 * K * w * sizeof(uint32_t), s));
+        CU(launch_augment_ell(dsm->D, (int)(2 * K), n, np, w, dsm->D_nnz, dsm->D_words, s));
         ctx->launches++;
     }
     // objective data (dense Q per instance), staged in pinned memory
@@ -971,8 +991,7 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     p.n_dir = (int)K;
     p.dirs = dsm->D;
     p.nnz = dsm->D_nnz;
-    p.col = dsm->D_col;
-    p.val = dsm->D_val;
+    p.words = dsm->D_words;
     p.nzmax = dsm->D_nzmax;
     p.Q = ctx->aQ.as<double>();
     p.c = ctx->ac.as<double>();

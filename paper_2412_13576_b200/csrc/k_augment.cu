@@ -20,22 +20,28 @@ namespace maple {
 
 namespace {
 
-constexpr int kAugThreads = 256;
+constexpr int kAugThreads = 1024;   // the most threads a CTA runs (large sets: memory-level parallelism)
 constexpr int kMaxN = 1024;
 
-// ELL of D: for each row e, its nnz[e] (<= width, the check kernel's bound over the set) columns in ascending
-// order and their values
-__global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int width, int16_t* col,
-                                int8_t* val, int32_t* nnz) {
+// ELL of D, slot-major: word[a * nD + e] = column | (uint8)value << 16 | END << 24 for the a-th nonzero of row e
+// (columns ascending; END marks the row's last nonzero), so a warp scanning 32 consecutive directions reads one
+// coalesced 128-byte line per slot; nnz[e] = the row's nonzero count (<= width, the compact kernel's bound)
+constexpr uint32_t kEnd = 1u << 24;
+__device__ __forceinline__ int wcol(uint32_t w) { return (int)(w & 0xFFFFu); }
+__device__ __forceinline__ int wval(uint32_t w) { return (int)(int8_t)(w >> 16); }
+
+__global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, int n_pad, int width,
+                                uint32_t* __restrict__ words, int32_t* __restrict__ nnz) {
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nD; e += gridDim.x * blockDim.x) {
         const int8_t* g = dirs + (size_t)e * n_pad;
-        int c = 0;
+        int c = 0, last = -1;
         for (int i = 0; i < n; ++i)
             if (g[i] && c < width) {
-                col[(size_t)e * width + c] = (int16_t)i;
-                val[(size_t)e * width + c] = g[i];
+                if (last >= 0) words[(size_t)(c - 1) * nD + e] = (uint32_t)last | ((uint32_t)(uint8_t)g[last] << 16);
+                last = i;
                 ++c;
             }
+        if (last >= 0) words[(size_t)(c - 1) * nD + e] = (uint32_t)last | ((uint32_t)(uint8_t)g[last] << 16) | kEnd;
         nnz[e] = c;
     }
 }
@@ -49,13 +55,15 @@ __global__ void qg_kernel(AugmentParams p) {
         const int e = (int)(t % nD);
         const double* Q = p.Q + (size_t)inst * p.n * p.n;
         const int k = p.nnz[e];
-        const int16_t* cl = p.col + (size_t)e * p.nzmax;
-        const int8_t* vl = p.val + (size_t)e * p.nzmax;
         double acc = 0.0;
         for (int a = 0; a < k; ++a) {
+            const uint32_t wa = p.words[(size_t)a * nD + e];
             double row = 0.0;
-            for (int b = 0; b < k; ++b) row += Q[(size_t)cl[a] * p.n + cl[b]] * (double)vl[b];
-            acc += (double)vl[a] * row;
+            for (int b = 0; b < k; ++b) {
+                const uint32_t wb = p.words[(size_t)b * nD + e];
+                row += Q[(size_t)wcol(wa) * p.n + wcol(wb)] * (double)wval(wb);
+            }
+            acc += (double)wval(wa) * row;
         }
         const_cast<double*>(p.qg)[(size_t)inst * nD + e] = acc;
     }
@@ -73,9 +81,10 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
     return a.lam < b.lam;
 }
 
-__global__ void __launch_bounds__(kAugThreads)
+__global__ void __launch_bounds__(kAugThreads, 1)
 augment_kernel(AugmentParams p, int staged) {
     __shared__ int32_t x[kMaxN];
+    __shared__ int32_t up[kMaxN], dn[kMaxN];   // room to the bounds: u - x, x - l
     __shared__ double grad[kMaxN];
     __shared__ Cand wbest[kAugThreads / 32];
     __shared__ Cand best_sh;
@@ -92,22 +101,21 @@ augment_kernel(AugmentParams p, int staged) {
         const int nD2 = 2 * p.n_dir, nz = p.nzmax;
         double* s_qg = reinterpret_cast<double*>(dsm);
         int32_t* s_nnz = reinterpret_cast<int32_t*>(s_qg + nD2);
-        int16_t* s_col = reinterpret_cast<int16_t*>(s_nnz + nD2);
-        int8_t* s_val = reinterpret_cast<int8_t*>(s_col + (size_t)nD2 * nz);
+        uint32_t* s_w = reinterpret_cast<uint32_t*>(s_nnz + nD2);
         for (int e = threadIdx.x; e < nD2; e += blockDim.x) {
             s_qg[e] = qg[e];
             s_nnz[e] = p.nnz[e];
         }
-        for (int e = threadIdx.x; e < nD2 * nz; e += blockDim.x) {
-            s_col[e] = p.col[e];
-            s_val[e] = p.val[e];
-        }
+        for (int e = threadIdx.x; e < nD2 * nz; e += blockDim.x) s_w[e] = p.words[e];
         qg = s_qg;
         p.nnz = s_nnz;
-        p.col = s_col;
-        p.val = s_val;
+        p.words = s_w;
     }
-    for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = xg[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        x[i] = xg[i];
+        up[i] = p.hi[i] - x[i];
+        dn[i] = x[i] - p.lo[i];
+    }
     __syncthreads();
     // ∇ = Q x + c ; 2 f(x) = x^T Q x + 2 c^T x + 2 c0
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -128,18 +136,24 @@ augment_kernel(AugmentParams p, int staged) {
     for (; it < p.max_iter; ++it) {
         Cand mine{DBL_MAX, 0x7fffffff, 0x7fffffff};
         for (int e = threadIdx.x; e < nD; e += blockDim.x) {
-            const int k = p.nnz[e];
-            const int16_t* cl = p.col + (size_t)e * p.nzmax;
-            const int8_t* vl = p.val + (size_t)e * p.nzmax;
-            double s = 0.0;
+            // step bound first, leaving at the first blocked coordinate (in a box most directions are blocked at
+            // an incumbent: a binary box blocks every g with a coordinate pushing past 0 or 1), then the score
+            const uint32_t* we = p.words + e;
             int lmax = 0x7fffffff;
-            for (int a = 0; a < k; ++a) {
-                const int i = cl[a], gi = vl[a];
-                s += (double)gi * grad[i];
-                const int room = gi > 0 ? (p.hi[i] - x[i]) / gi : (x[i] - p.lo[i]) / (-gi);
+            for (int a = 0;; ++a) {
+                const uint32_t w = we[(size_t)a * nD];
+                const int i = wcol(w), gi = wval(w);
+                const int room = gi == 1 ? up[i] : gi == -1 ? dn[i] : gi > 0 ? up[i] / gi : dn[i] / (-gi);
                 lmax = min(lmax, room);
+                if (lmax < 1 || (w & kEnd)) break;
             }
-            if (lmax < 1 || lmax == 0x7fffffff) continue;
+            if (lmax < 1) continue;
+            double s = 0.0;
+            for (int a = 0;; ++a) {
+                const uint32_t w = we[(size_t)a * nD];
+                s += (double)wval(w) * grad[wcol(w)];
+                if (w & kEnd) break;
+            }
             const double q = qg[e];
             for (int lam = 1; lam <= lmax; ++lam) {
                 const double dl = (double)lam;
@@ -170,16 +184,24 @@ augment_kernel(AugmentParams p, int staged) {
         const Cand b = best_sh;
         if (b.e == 0x7fffffff) break;  // no improving step: x is Graver-optimal w.r.t. D
         const int k = p.nnz[b.e];
-        const int16_t* cl = p.col + (size_t)b.e * p.nzmax;
-        const int8_t* vl = p.val + (size_t)b.e * p.nzmax;
-        // ∇ += λ Q g (Q symmetric: column cl[a] of Q = row cl[a], read coalesced)
+        const uint32_t* wb = p.words + b.e;
+        // ∇ += λ Q g (Q symmetric: column i of Q = row i, read coalesced)
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             double acc = 0.0;
-            for (int a = 0; a < k; ++a) acc += Q[(size_t)cl[a] * n + i] * (double)vl[a];
+            for (int a = 0; a < k; ++a) {
+                const uint32_t w = wb[(size_t)a * nD];
+                acc += Q[(size_t)wcol(w) * n + i] * (double)wval(w);
+            }
             grad[i] += (double)b.lam * acc;
         }
         __syncthreads();
-        for (int a = threadIdx.x; a < k; a += blockDim.x) x[cl[a]] += b.lam * (int)vl[a];
+        for (int a = threadIdx.x; a < k; a += blockDim.x) {
+            const uint32_t w = wb[(size_t)a * nD];
+            const int i = wcol(w), dx = b.lam * wval(w);
+            x[i] += dx;
+            up[i] -= dx;
+            dn[i] += dx;
+        }
         if (threadIdx.x == 0) f2_sh += b.key;
         __syncthreads();
     }
@@ -237,11 +259,11 @@ __global__ void best_kernel(AugmentParams p, int32_t* xbest, double* f2best, int
 
 }  // namespace
 
-cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, int16_t* col,
-                               int8_t* val, cudaStream_t s) {
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, uint32_t* words,
+                               cudaStream_t s) {
     if (nD <= 0) return cudaSuccess;
     const unsigned blocks = (unsigned)std::min(148 * 8, (nD + 255) / 256);
-    ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, width, col, val, nnz);
+    ell_fill_kernel<<<blocks, 256, 0, s>>>(dirs, nD, n, n_pad, width, words, nnz);
     return cudaGetLastError();
 }
 
@@ -271,13 +293,14 @@ cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s) {
     const int64_t blocks = (int64_t)p.n_inst * p.k0;
     if (blocks <= 0) return cudaSuccess;
     const size_t nD2 = (size_t)2 * p.n_dir;
-    const size_t smem = nD2 * 8 + nD2 * 4 + nD2 * p.nzmax * 3 + 16;
+    const size_t smem = nD2 * 8 + nD2 * 4 + nD2 * p.nzmax * 4 + 16;
     const int staged = smem <= 96 * 1024;
     if (staged) {   // dynamic + ~12 KB static may pass the 48 KB default even when the dynamic part does not
         cudaError_t e = cudaFuncSetAttribute(augment_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    augment_kernel<<<(unsigned)blocks, kAugThreads, staged ? smem : 0, s>>>(p, staged);
+    const int threads = nD2 > 16384 ? kAugThreads : 256;
+    augment_kernel<<<(unsigned)blocks, threads, staged ? smem : 0, s>>>(p, staged);
     return cudaGetLastError();
 }
 

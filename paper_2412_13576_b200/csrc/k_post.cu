@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
             fw.l1[r] = ok ? l1 : -1;
             // thermometer code: coordinate i owns bits [off_i, off_i + u_i - l_i) of each half
             uint32_t* code = fw.codes + (size_t)r * W2;
+            uint32_t f0 = 0u, f1 = 0u, f2 = 0u, f3 = 0u;   // 64-bit folds of P and N (bit i mod 64), the filter's prefilter
             if (fw.binary && ok) {  // bit i of P = [g_i > 0], of N = [g_i < 0] (off_i = i)
                 const uint32_t* gw = reinterpret_cast<const uint32_t*>(g);
                 for (int w = 0; w < fw.Wh; ++w) {
@@ -190,6 +191,13 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
                     }
                     code[w] = pw;
                     code[fw.Wh + w] = nw_;
+                    if (w & 1) {
+                        f1 |= pw;
+                        f3 |= nw_;
+                    } else {
+                        f0 |= pw;
+                        f2 |= nw_;
+                    }
                 }
             } else
             for (int hf = 0; hf < 2; ++hf) {
@@ -203,8 +211,14 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
                         if (a < e) word |= (e - a == 32) ? 0xFFFFFFFFu : (((1u << (e - a)) - 1u) << a);
                     }
                     code[hf * fw.Wh + w] = word;
+                    if (hf) {
+                        if (w & 1) f3 |= word; else f2 |= word;
+                    } else {
+                        if (w & 1) f1 |= word; else f0 |= word;
+                    }
                 }
             }
+            fw.sig[r] = make_uint4(f0, f1, f2, f3);
         }
     }
     if (bad) atomicAdd(n_bad, bad);
@@ -268,17 +282,18 @@ __global__ void scatter_kernel(const int32_t* l1, const unsigned long long* dcou
 }
 
 constexpr int kFilterThreads = 256;
-constexpr int kTile = 256;
+constexpr int kTile = 512;
 
 // Dominance test. Rows are visited in L1 order (order[], level_start[]); a block takes 256 consecutive
 // positions and streams the candidate dominators (all rows of strictly smaller L1) through shared memory
-// tile by tile, each thread stopping at its first dominator; the block stops when all its rows are decided.
+// tile by tile as (64-bit folds of P and N, row) — the fold test is a necessary condition for h ⊑ g and for h ⊑ -g;
+// the exact test on the full codes runs only for pairs that pass it. Each thread stops at its first
+// dominator; the block stops when all its rows are decided.
 template <int WH>
 __global__ void __launch_bounds__(kFilterThreads)
 dominance_kernel(FilterWork fw) {
-    extern __shared__ __align__(16) uint32_t dyn_sh[];
-    uint32_t* tile = dyn_sh;                                         // kTile x 2WH code words
-    int32_t* tile_row = reinterpret_cast<int32_t*>(dyn_sh + kTile * 2 * WH);
+    __shared__ uint4 tile_sig[kTile];
+    __shared__ int32_t tile_row[kTile];
     __shared__ int32_t smax;
     const int Wh = fw.Wh;
     const int W2 = 2 * Wh;
@@ -289,6 +304,7 @@ dominance_kernel(FilterWork fw) {
         const bool active0 = pos < n_valid;
         int32_t row = -1, limit = 0;
         uint32_t P[WH], N[WH];
+        uint32_t fp0 = 0, fp1 = 0, fn0 = 0, fn1 = 0;
         if (active0) {
             row = fw.order[pos];
             limit = fw.level_start[fw.l1[row]];  // rows with strictly smaller L1
@@ -296,6 +312,13 @@ dominance_kernel(FilterWork fw) {
             for (int w = 0; w < WH; ++w) {
                 P[w] = w < Wh ? fw.codes[(size_t)row * W2 + w] : 0u;
                 N[w] = w < Wh ? fw.codes[(size_t)row * W2 + Wh + w] : 0u;
+                if (w & 1) {
+                    fp1 |= P[w];
+                    fn1 |= N[w];
+                } else {
+                    fp0 |= P[w];
+                    fn0 |= N[w];
+                }
             }
         }
         bool done = !active0 || limit == 0;
@@ -303,7 +326,8 @@ dominance_kernel(FilterWork fw) {
         __syncthreads();
         if (threadIdx.x == 0) smax = 0;
         __syncthreads();
-        if (active0) atomicMax(&smax, limit);
+        const int32_t scan = min(limit, fw.scan_cap);   // the rows this thread scans here (a prefix of its dominators)
+        if (active0) atomicMax(&smax, scan);
         __syncthreads();
         const int32_t maxlim = smax;
         for (int32_t t0 = 0; t0 < maxlim; t0 += kTile) {
@@ -312,36 +336,211 @@ dominance_kernel(FilterWork fw) {
                 const int32_t q = t0 + i;
                 const int32_t hr = q < maxlim ? fw.order[q] : -1;
                 tile_row[i] = hr;
-                for (int w = 0; w < 2 * WH; ++w) {
-                    const int half = w >= WH, ww = half ? w - WH : w;   // smem: P words [0,WH), N words [WH,2WH)
-                    tile[i * 2 * WH + w] = (hr >= 0 && ww < Wh) ? fw.codes[(size_t)hr * W2 + half * Wh + ww] : 0u;
-                }
+                tile_sig[i] = hr >= 0 ? fw.sig[hr] : make_uint4(~0u, ~0u, ~0u, ~0u);
             }
             __syncthreads();
             if (!done) {
-                const int lim = min(kTile, limit - t0);
+                const int lim = min(kTile, scan - t0);
                 for (int i = 0; i < lim; ++i) {
-                    const uint32_t* hc = &tile[i * 2 * WH];
+                    const uint4 hs = tile_sig[i];
+                    const uint32_t pv = (hs.x & ~fp0) | (hs.y & ~fp1) | (hs.z & ~fn0) | (hs.w & ~fn1);
+                    const uint32_t nv = (hs.x & ~fn0) | (hs.y & ~fn1) | (hs.z & ~fp0) | (hs.w & ~fp1);
+                    if (pv != 0u && nv != 0u) continue;
+                    const int32_t hr = tile_row[i];
+                    const uint32_t* hc = fw.codes + (size_t)hr * W2;
                     uint32_t pos_v = 0, neg_v = 0;
 #pragma unroll
                     for (int w = 0; w < WH; ++w) {
-                        const uint32_t hp = hc[w], hn = hc[WH + w];
-                        pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
-                        neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
+                        if (w < Wh) {
+                            const uint32_t hp = hc[w], hn = hc[Wh + w];
+                            pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
+                            neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
+                        }
                     }
                     if (pos_v == 0u || neg_v == 0u) {
                         done = true;
-                        wit = tile_row[i];
+                        wit = hr;
                         break;
                     }
                 }
-                if (t0 + kTile >= limit) done = true;
+                if (t0 + kTile >= scan) done = true;
             }
             __syncthreads();
         }
-        if (active0) {
-            fw.keep[row] = (wit < 0) ? 1 : 0;
+        const bool undec = active0 && wit < 0 && scan < limit;
+        if (active0) {   // 2: not dominated by the scanned prefix, which is not all of its candidates (undecided)
+            fw.keep[row] = (wit >= 0) ? 0 : (undec ? 2 : 1);
             fw.witness[row] = wit;
+        }
+        const int nu = __syncthreads_count(undec);
+        if (threadIdx.x == 0 && nu) atomicAdd(fw.n_undec, nu);
+    }
+}
+
+// ---- indexed filter (large pools) ----
+// h ⊑ ±g requires supp(h) ⊆ supp(g). Every valid row h is filed under one key coordinate κ(h) ∈ supp(h) — its
+// rarest coordinate over the pool (ties: lowest index) — and, inside that list, by its L1 norm: bin
+// κ(h)·(Lmax+1) + L1(h). A row g then only meets the rows filed under its own support coordinates with a
+// strictly smaller L1: for c ∈ supp(g) the contiguous range [bin(c, 0), bin(c, L1(g))). Each such pair is
+// tested by the 64-bit folds first and then exactly on the codes, as in the tiled kernel; the keep bit is the
+// same (it is defined pairwise), only the recorded witness may differ.
+constexpr int kIdxMaxN = 1024;
+
+// thread per row (16-byte loads of its bytes); every kernel of the index returns at once when the tiled prefix
+// scan left no row undecided
+__global__ void coord_freq_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap) {
+    if (*fw.n_undec == 0) return;
+    __shared__ int32_t sf[kIdxMaxN];
+    for (int i = threadIdx.x; i < fw.n; i += blockDim.x) sf[i] = 0;
+    __syncthreads();
+    const int64_t count = dev_count(dcount, cap);
+    const int nw = fw.n_pad / 16;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        if (fw.l1[r] < 0) continue;
+        const int4* g = reinterpret_cast<const int4*>(fw.rows + (size_t)r * fw.n_pad);
+        for (int w = 0; w < nw; ++w) {
+            const int4 v = g[w];
+            const uint32_t q[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                if ((q[b >> 2] >> (8 * (b & 3))) & 0xFFu) atomicAdd(&sf[16 * w + b], 1);   // padding bytes are 0
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < fw.n; i += blockDim.x)
+        if (sf[i]) atomicAdd(&fw.freq[i], sf[i]);
+}
+
+__global__ void key_bin_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap) {
+    if (*fw.n_undec == 0) return;
+    __shared__ int32_t sf[kIdxMaxN];
+    for (int i = threadIdx.x; i < fw.n; i += blockDim.x) sf[i] = fw.freq[i];
+    __syncthreads();
+    const int64_t count = dev_count(dcount, cap);
+    const int nw = fw.n_pad / 16;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        const int l1 = fw.l1[r];
+        if (l1 < 0) continue;
+        const int4* g = reinterpret_cast<const int4*>(fw.rows + (size_t)r * fw.n_pad);
+        // lowest (freq, index) over the support: freq (< 2^31) and index packed into one 64-bit key
+        unsigned long long best = ~0ULL;
+        for (int w = 0; w < nw; ++w) {
+            const int4 v = g[w];
+            const uint32_t q[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                if ((q[b >> 2] >> (8 * (b & 3))) & 0xFFu) {
+                    const int i = 16 * w + b;
+                    best = min(best, ((unsigned long long)(uint32_t)sf[i] << 32) | (uint32_t)i);
+                }
+        }
+        const int bin = (int)(best & 0xFFFFFFFFu) * (fw.Lmax + 1) + l1;
+        fw.key_bin[r] = bin;
+        atomicAdd(&fw.bin_hist[bin], 1);
+    }
+}
+
+// exclusive scan of bin_hist[0, nb) into bin_start[0, nb] and bin_cursor[0, nb): one block, chunk per thread
+__global__ void __launch_bounds__(1024) bin_scan_kernel(FilterWork fw, int nb) {
+    if (*fw.n_undec == 0) return;
+    __shared__ int32_t part[1024];
+    const int t = threadIdx.x;
+    const int chunk = (nb + 1023) / 1024;
+    const int b0 = min(nb, t * chunk), b1 = min(nb, b0 + chunk);
+    int32_t acc = 0;
+    for (int b = b0; b < b1; ++b) acc += fw.bin_hist[b];
+    part[t] = acc;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {   // Hillis-Steele inclusive scan of the partial sums
+        const int32_t v = t >= off ? part[t - off] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - acc;
+    for (int b = b0; b < b1; ++b) {
+        fw.bin_start[b] = run;
+        fw.bin_cursor[b] = run;
+        run += fw.bin_hist[b];
+    }
+    if (t == 1023) fw.bin_start[nb] = part[1023];
+}
+
+__global__ void bin_scatter_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap) {
+    if (*fw.n_undec == 0) return;
+    const int64_t count = dev_count(dcount, cap);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        if (fw.l1[r] < 0) continue;
+        const int32_t pos = atomicAdd(&fw.bin_cursor[fw.key_bin[r]], 1);
+        fw.list_row[pos] = (int32_t)r;
+        fw.list_sig[pos] = fw.sig[r];
+    }
+}
+
+// warp per row g: scan the lists of g's support coordinates (lanes stride each range), stop at the first
+// dominator found by any lane
+constexpr int kIdxThreads = 256;
+template <int WH>
+__global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork fw, const unsigned long long* dcount,
+                                                                   int64_t cap) {
+    if (*fw.n_undec == 0) return;
+    __shared__ uint32_t gcode[kIdxThreads / 32][2 * WH];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int Wh = fw.Wh, W2 = 2 * Wh;
+    const int64_t count = dev_count(dcount, cap);
+    const int64_t warp0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t* P = gcode[wib];
+    uint32_t* N = P + WH;
+    for (int64_t r = warp0; r < count; r += nwarps) {
+        if (fw.keep[r] != 2) continue;   // decided by the tiled prefix scan (or invalid)
+        const int l1 = fw.l1[r];
+        __syncwarp();
+        for (int w = lane; w < Wh; w += 32) {
+            P[w] = fw.codes[(size_t)r * W2 + w];
+            N[w] = fw.codes[(size_t)r * W2 + Wh + w];
+        }
+        const uint4 gs = fw.sig[r];
+        __syncwarp();
+        const int8_t* g = fw.rows + (size_t)r * fw.n_pad;
+        int32_t wit = -1;
+        for (int i0 = 0; i0 < fw.n && wit < 0; i0 += 32) {
+            const int i = i0 + lane;
+            unsigned nzm = __ballot_sync(0xffffffffu, i < fw.n && g[i] != 0);
+            while (nzm && wit < 0) {
+                const int c = i0 + __ffs(nzm) - 1;
+                nzm &= nzm - 1;
+                const int bin0 = c * (fw.Lmax + 1);
+                const int32_t lo = fw.bin_start[bin0], hi = fw.bin_start[bin0 + l1];
+                for (int32_t p0 = lo; p0 < hi; p0 += 32) {
+                    const int32_t p = p0 + lane;
+                    bool found = false;
+                    if (p < hi) {
+                        const uint4 hs = fw.list_sig[p];
+                        const uint32_t pv = (hs.x & ~gs.x) | (hs.y & ~gs.y) | (hs.z & ~gs.z) | (hs.w & ~gs.w);
+                        const uint32_t nv = (hs.x & ~gs.z) | (hs.y & ~gs.w) | (hs.z & ~gs.x) | (hs.w & ~gs.y);
+                        if (pv == 0u || nv == 0u) {
+                            const uint32_t* hc = fw.codes + (size_t)fw.list_row[p] * W2;
+                            uint32_t pos_v = 0, neg_v = 0;
+                            for (int w = 0; w < Wh; ++w) {
+                                const uint32_t hp = hc[w], hn = hc[Wh + w];
+                                pos_v |= (hp & ~P[w]) | (hn & ~N[w]);
+                                neg_v |= (hp & ~N[w]) | (hn & ~P[w]);
+                            }
+                            found = pos_v == 0u || neg_v == 0u;
+                        }
+                    }
+                    const unsigned fm = __ballot_sync(0xffffffffu, found);
+                    if (fm) {
+                        wit = fw.list_row[p0 + __ffs(fm) - 1];
+                        break;
+                    }
+                }
+            }
+        }
+        if (lane == 0) {
+            fw.keep[r] = wit < 0 ? 1 : 0;
+            fw.witness[r] = wit;
         }
     }
 }
@@ -563,14 +762,8 @@ cudaError_t launch_check_codes(const int8_t* rows, const unsigned long long* dco
     return cudaGetLastError();
 }
 
-cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const uint8_t* valid, FilterWork& fw,
-                          int filter_minimal, cudaStream_t s, int* launches) {
-    if (cap <= 0) return cudaSuccess;
-    if (!filter_minimal) {
-        keep_valid_kernel<<<grid_for(cap), 256, 0, s>>>(valid, dcount, cap, fw.keep, fw.witness);
-        *launches += 1;
-        return cudaGetLastError();
-    }
+static cudaError_t launch_filter_tiled(const unsigned long long* dcount, int64_t cap, FilterWork& fw, cudaStream_t s,
+                                       int* launches) {
     cudaError_t e;
     const int nb = fw.Lmax + 1;
     if ((e = cudaMemsetAsync(fw.hist, 0, sizeof(int32_t) * (fw.Lmax + 2), s)) != cudaSuccess) return e;
@@ -583,16 +776,49 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
     const unsigned blocks = grid_for(cap, kFilterThreads, 148 * 4);
 #define MAPLE_DOM(WHV)                                                                                       \
     if (fw.Wh <= WHV) {                                                                                      \
-        const size_t sm = (size_t)kTile * (2 * WHV + 1) * 4;                                                 \
-        if ((e = cudaFuncSetAttribute(dominance_kernel<WHV>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                      (int)sm)) != cudaSuccess)                                              \
-            return e;                                                                                        \
-        dominance_kernel<WHV><<<blocks, kFilterThreads, sm, s>>>(fw);                                        \
+        dominance_kernel<WHV><<<blocks, kFilterThreads, 0, s>>>(fw);                                         \
     } else
     MAPLE_DOM(1) MAPLE_DOM(2) MAPLE_DOM(4) MAPLE_DOM(8) MAPLE_DOM(16) MAPLE_DOM(32) return cudaErrorInvalidValue;
 #undef MAPLE_DOM
     *launches += 1;
     return cudaGetLastError();
+}
+
+
+cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const uint8_t* valid, FilterWork& fw,
+                          int filter_minimal, cudaStream_t s, int* launches) {
+    if (cap <= 0) return cudaSuccess;
+    if (!filter_minimal) {
+        keep_valid_kernel<<<grid_for(cap), 256, 0, s>>>(valid, dcount, cap, fw.keep, fw.witness);
+        *launches += 1;
+        return cudaGetLastError();
+    }
+    cudaError_t e;
+    const int algo = fw.algo;
+    fw.scan_cap = algo == 2 ? 2 * kTile : 0x7fffffff;
+    if ((e = cudaMemsetAsync(fw.n_undec, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
+    if ((e = launch_filter_tiled(dcount, cap, fw, s, launches)) != cudaSuccess) return e;
+    if (algo == 2) {   // rows the prefix did not decide: indexed by key coordinate and L1
+        if (fw.n > kIdxMaxN) return cudaErrorInvalidValue;
+        const int nbins = fw.n * (fw.Lmax + 1);
+        if ((e = cudaMemsetAsync(fw.freq, 0, sizeof(int32_t) * fw.n, s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(fw.bin_hist, 0, sizeof(int32_t) * nbins, s)) != cudaSuccess) return e;
+        coord_freq_kernel<<<grid_for(cap, 256, 148 * 4), 256, 0, s>>>(fw, dcount, cap);
+        key_bin_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(fw, dcount, cap);
+        bin_scan_kernel<<<1, 1024, 0, s>>>(fw, nbins);
+        bin_scatter_kernel<<<grid_for(cap), 256, 0, s>>>(fw, dcount, cap);
+        *launches += 4;
+        const unsigned blocks = grid_for((cap + 7) / 8, kIdxThreads, 148 * 8);
+#define MAPLE_IDX(WHV)                                                                 \
+        if (fw.Wh <= WHV) {                                                            \
+            dominance_idx_kernel<WHV><<<blocks, kIdxThreads, 0, s>>>(fw, dcount, cap); \
+        } else
+        MAPLE_IDX(2) MAPLE_IDX(8) MAPLE_IDX(32) return cudaErrorInvalidValue;
+#undef MAPLE_IDX
+        *launches += 1;
+        return cudaGetLastError();
+    }
+    return cudaSuccess;
 }
 
 cudaError_t launch_signed_merge(const int8_t* S, int64_t k, int n, int n_pad, int8_t* out, cudaStream_t s) {

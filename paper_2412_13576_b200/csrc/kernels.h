@@ -93,6 +93,18 @@ struct FilterWork {
     uint8_t* keep;                // count
     int32_t* witness;             // count
     int Lmax;
+    uint4* sig;                   // count: 64-bit folds (bit i mod 64) of the two code halves (the filter's prefilter)
+    int algo;                     // 1: tiled scan of all lower-L1 rows; 2: tiled prefix, then indexed by key coordinate
+    int scan_cap;                 // tiled scan: rows of smaller L1 scanned per row (set by launch_filter)
+    const int8_t* rows;           // the rows themselves (stride n_pad): supports, for the indexed filter
+    int32_t* freq;                // n: rows having coordinate i in their support
+    int32_t* key_bin;             // count: key coordinate * (Lmax + 1) + L1
+    int32_t* bin_hist;            // n * (Lmax + 1)
+    int32_t* bin_start;           // n * (Lmax + 1) + 1
+    int32_t* bin_cursor;          // n * (Lmax + 1)
+    int32_t* list_row;            // count: rows in bin order
+    uint4* list_sig;              // count: their folds, in bin order
+    int32_t* n_undec;             // rows the tiled prefix left undecided (the index is built only if > 0)
 };
 // flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= u - l (conditions C1-C3), for the first
 // min(*dcount, cap) rows; with encode != 0 also the filter's thermometer codes and L1 norms.
@@ -139,8 +151,7 @@ struct AugmentParams {
     int n_dir;                    // canonical directions K; D = ±, sorted lexicographically: 2K entries
     const int8_t* dirs;           // D, 2K x n_pad (lex sorted, both signs)
     const int32_t* nnz;           // ELL of D: nonzeros per row (2K)
-    const int16_t* col;           // 2K x nzmax column indices (ascending)
-    const int8_t* val;            // 2K x nzmax values
+    const uint32_t* words;        // nzmax x 2K, slot-major: column | (uint8)value << 16 | END << 24 (columns ascending)
     int nzmax;
     const double* Q;              // n x n (per instance: Q + inst * n * n)
     const double* c;              // n (per instance)
@@ -156,9 +167,9 @@ struct AugmentParams {
 };
 cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s);
 cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s);
-// ELL form of the 2K rows of D into col / val (nD x width, width >= every row's nonzero count) and nnz
-cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, int16_t* col,
-                               int8_t* val, cudaStream_t s);
+// slot-major ELL words of the 2K rows of D (width x nD, width >= every row's nonzero count) and nnz
+cudaError_t launch_augment_ell(const int8_t* dirs, int nD, int n, int n_pad, int width, int32_t* nnz, uint32_t* words,
+                               cudaStream_t s);
 cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* f2best, cudaStream_t s);
 // D = S ∪ -S in lexicographic order from a lexicographically sorted canonical S (a merge; 2k rows into out)
 cudaError_t launch_signed_merge(const int8_t* S, int64_t k, int n, int n_pad, int8_t* out, cudaStream_t s);

@@ -63,6 +63,7 @@ _SIGS = [
     ("maple_kernel_launches", C.c_int64, [_P]),
     ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
     ("maple_descent_kernel", C.c_int, [_P]),
+    ("maple_set_filter_algorithm", C.c_int, [_P, C.c_int32]),
     ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
     ("maple_feasible_starts", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, _P,
                                         C.c_int32, _P, _P]),
@@ -217,6 +218,10 @@ class Context:
 
     def set_descent_kernel(self, which: int):
         _check(_lib.maple_set_descent_kernel(self.h, which), self.h)
+
+    def set_filter_algorithm(self, which: int):
+        """0 auto, 1 tiled, 2 indexed (maple_set_filter_algorithm): same kept set, different pair enumeration."""
+        _check(_lib.maple_set_filter_algorithm(self.h, which), self.h)
 
     @property
     def descent_kernel(self) -> str:

@@ -254,3 +254,21 @@ def test_tc_two_and_four_threads_per_start_bit_identical(gpu_lib, name):
     ra = a.extract(3000, inst.steps, inst.lr, 5).rows()
     rb = b.extract(3000, inst.steps, inst.lr, 5).rows()
     np.testing.assert_array_equal(ra, rb)
+
+
+@pytest.mark.parametrize("name,N", [("C1", 1024), ("C2a", 8192), ("C2b", 8192), ("C3", 4096)])
+def test_filter_algorithms_identical(gpu_lib, name, N):
+    """The tiled and the indexed ⊑ filter enumerate different pairs but decide the same pairwise property:
+    identical kept sets (bit for bit), and G1 against the oracle on the GPU candidates for the indexed one."""
+    from synth import config
+    inst = config(name)
+    ctx = _ctx(gpu_lib, inst)
+    out = []
+    for algo in (1, 2):
+        ctx.set_filter_algorithm(algo)
+        ctx.set_debug(True)
+        out.append(ctx.extract(N, inst.steps, inst.lr, inst.seed).rows())
+    np.testing.assert_array_equal(out[0], out[1])
+    if name == "C1":   # (the other shapes' G1 tests run through the auto = indexed filter)
+        ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, ctx.candidates())
+        assert nbad == 0 and [tuple(r) for r in out[1].tolist()] == ref
