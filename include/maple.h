@@ -200,6 +200,13 @@ int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
 /* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05;
  * negative error code for a null context. Host only. */
 int maple_descent_kernel(const maple_ctx* ctx);
+/* Descent variants (DESIGN readings #24-#25). Alg. 3 line 8 updates z with "first-order
+ * methods such as Adam": optimizer 0 = Adam (default, torch.optim.Adam formula), 1 = plain gradient descent
+ * z <- z - step_size * g, 2 = sign gradient descent z <- z - step_size * sign(g) (sign(0) = 0), g the Eq. 3
+ * subgradient. harvest_final = 1 applies Alg. 3 lines 9-10 to the final iterate z_T only (0: after
+ * every step, the paper's loop). The 4-thread tcgen05 kernel implements the default only: a variant extraction
+ * with descent kernel 3 selected runs kernel 2. Returns BAD_ARG for a null context or out-of-range values. Host only. */
+int maple_set_descent_variant(maple_ctx* ctx, int32_t optimizer, int32_t harvest_final);
 /* Select the ⊑-minimality filter's pair enumeration (Def. 1-2; the kept set is the same for all):
  * 0 = auto (indexed when n <= 1024), 1 = tiled (every row against all rows of smaller L1 norm), 2 = indexed
  * (every row against the rows filed under one of its support coordinates with smaller L1 norm; needs n <= 1024).

@@ -16,6 +16,9 @@ Readings:
   #6    ⌈·⌋ rounds half away from zero.
   #11/#12 harvest after each update t = 1..T; g = 0 is excluded.
   #13   set semantics with one canonical representative per ± pair (first nonzero > 0).
+  #24   optimizer variants ("first-order methods such as Adam"): plain GD
+        z <- z - lr g and sign-GD z <- z - lr sign(g) (sign(0) = 0), lr rounded once to the working dtype.
+  #25   harvest-final-only variant: Alg. 3 line 9 applied to the final iterate z_T only.
 """
 from __future__ import annotations
 
@@ -112,10 +115,15 @@ def harvest(Z, B, l, u):
     return canonicalize_rows(G[keep])
 
 
+OPTIMIZERS = ("adam", "gd", "signgd")
+
+
 def descend(z0, B, steps, lr, lam1=0.85, lam2=1.0, beta1=0.9, beta2=0.999, eps=1e-8, dtype=np.float64,
-            l=None, u=None, pool=None, trace=None):
+            l=None, u=None, pool=None, trace=None, optimizer="adam", harvest_final=False):
     """Alg. 3 lines 6-11 for a batch of starts. Returns the final iterates Z (dtype). If l, u and `pool`
-    (a set) are given, every step's harvest is added to the pool as canonical int tuples.
+    (a set) are given, every step's harvest (only the last one with harvest_final, reading #25) is added to
+    the pool as canonical int tuples. `optimizer` selects line 8's update (reading #24): "adam" (default),
+    "gd" (z - lr g) or "signgd" (z - lr sign(g)).
 
     Scalars follow torch.optim.Adam (reading #9; PyTorch 2.1.0): beta, 1 - beta, the step size
     lr / (1 - beta1^t) and sqrt(1 - beta2^t) are computed in Python double and then used in `dtype`
@@ -127,17 +135,25 @@ def descend(z0, B, steps, lr, lam1=0.85, lam2=1.0, beta1=0.9, beta2=0.999, eps=1
     v = np.zeros_like(Z)
     b1, b2 = dt.type(beta1), dt.type(beta2)
     omb1, omb2 = dt.type(1.0 - beta1), dt.type(1.0 - beta2)
+    if optimizer not in OPTIMIZERS:
+        raise ValueError(f"optimizer must be one of {OPTIMIZERS}")
+    lr_d = dt.type(lr)
     for t in range(1, steps + 1):
         G = subgrad(Z, Bd, lam1, lam2)
-        m = b1 * m + omb1 * G
-        v = b2 * v + omb2 * G * G
-        step = dt.type(lr / (1.0 - beta1 ** t))
-        bc2s = dt.type(np.sqrt(1.0 - beta2 ** t))
-        denom = np.sqrt(v) / bc2s + dt.type(eps)
-        Z = Z - step * m / denom
+        if optimizer == "adam":
+            m = b1 * m + omb1 * G
+            v = b2 * v + omb2 * G * G
+            step = dt.type(lr / (1.0 - beta1 ** t))
+            bc2s = dt.type(np.sqrt(1.0 - beta2 ** t))
+            denom = np.sqrt(v) / bc2s + dt.type(eps)
+            Z = Z - step * m / denom
+        elif optimizer == "gd":
+            Z = Z - lr_d * G
+        else:
+            Z = Z - lr_d * np.sign(G).astype(dt)
         if trace is not None:
             trace.append(Z.copy())
-        if pool is not None:
+        if pool is not None and (not harvest_final or t == steps):
             H = harvest(Z, B, np.asarray(l, np.int64), np.asarray(u, np.int64))
             if H.shape[0]:
                 for row in np.unique(H, axis=0):
@@ -146,7 +162,7 @@ def descend(z0, B, steps, lr, lam1=0.85, lam2=1.0, beta1=0.9, beta2=0.999, eps=1
 
 
 def extract_pool(B, Bplus, l, u, n_starts, steps, lr, seed, starts=None, dtype=np.float64,
-                 lam1=0.85, lam2=1.0, chunk=8192):
+                 lam1=0.85, lam2=1.0, chunk=8192, optimizer="adam", harvest_final=False):
     """Alg. 3 over global start indices `starts` (default range(n_starts)): the harvested direction
     set 𝒢 (canonical tuples, before the exact check / ⊑ filter) and the final iterates."""
     if starts is None:
@@ -159,6 +175,7 @@ def extract_pool(B, Bplus, l, u, n_starts, steps, lr, seed, starts=None, dtype=n
         _, z0 = sample_starts(l, u, Bplus, seed, idx)
         if np.dtype(dtype) == np.float32:
             z0 = z0.astype(np.float32)
-        finals.append(descend(z0, B, steps, lr, lam1=lam1, lam2=lam2, dtype=dtype, l=l, u=u, pool=pool))
+        finals.append(descend(z0, B, steps, lr, lam1=lam1, lam2=lam2, dtype=dtype, l=l, u=u, pool=pool,
+                              optimizer=optimizer, harvest_final=harvest_final))
     Z = np.concatenate(finals) if finals else np.zeros((0, np.asarray(B).shape[1]))
     return pool, Z

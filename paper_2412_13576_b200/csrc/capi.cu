@@ -110,6 +110,8 @@ struct maple_ctx {
     int filter_minimal = 1;
     int descent_kernel = 0;
     int filter_algo = 0;          // 0 auto (indexed), 1 tiled, 2 indexed
+    int optimizer = 0;            // reading #24: 0 Adam, 1 GD, 2 sign-GD
+    int harvest_final = 0;        // reading #25: 1 = harvest the final iterate only
     // workspace
     DevBuf ffreq, fkey, fbh, fbs, fbc, flrow, flsig;   // indexed filter (k_post.cu)
     DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, sig, l1, hist, level_start, cursor, order, keep,
@@ -381,6 +383,9 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.lo = ctx->dl.as<int32_t>();
     p.hi = ctx->du.as<int32_t>();
     p.box = ctx->dbox.as<int32_t>();
+    p.opt = ctx->optimizer;
+    p.harvest_final = ctx->harvest_final;
+    p.lr = (float)ctx->tab_lr;   // the step table was just built for this call's step size
     return p;
 }
 
@@ -389,7 +394,8 @@ constexpr int kAutoTc = 2;   // auto choice for tensor-core shapes
 // the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start)
 int which_descent(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
-    if (ctx->descent_kernel != 0) return ctx->descent_kernel;
+    const bool variant = ctx->optimizer != 0 || ctx->harvest_final != 0;
+    if (ctx->descent_kernel != 0) return (ctx->descent_kernel == 3 && variant) ? 2 : ctx->descent_kernel;
     return tc_ok ? kAutoTc : 1;
 }
 
@@ -676,6 +682,13 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
     if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
+    return MAPLE_OK;
+}
+
+int maple_set_descent_variant(maple_ctx* ctx, int32_t optimizer, int32_t harvest_final) {
+    if (!ctx || optimizer < 0 || optimizer > 2 || harvest_final < 0 || harvest_final > 1) return MAPLE_ERR_BAD_ARG;
+    ctx->optimizer = optimizer;
+    ctx->harvest_final = harvest_final;
     return MAPLE_OK;
 }
 

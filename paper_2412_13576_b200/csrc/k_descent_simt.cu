@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     __syncwarp();
 
     const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2, eps = p.eps;
+    const float lr = p.lr;
+    const int opt = p.opt;
     for (int t = 0; t < p.T; ++t) {
         // forward: s_i = sign((B z)_i)
         ell_run(wf, Lf, zsh, res + lane);
@@ -172,7 +174,9 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
         // penalties + Adam (reading #9) on this lane's coordinates; r = round(z) replaces Γ in grsh.
         // Branch-free: unused places update the scratch coordinate d (Γ = 0, z = 0: it stays 0).
         const float4 st = p.step_tab[t];
-        bool changed = (t == 0);   // the first iterate is always harvested (no previous round(z))
+        // the first iterate is always harvested (no previous round(z)); final-only mode (reading #25): the last
+        const bool final_step = t == p.T - 1;
+        bool changed = p.harvest_final ? final_step : (t == 0);
 #pragma unroll
         for (int q = 0; q < QD; ++q) {
             const int j = jq[q * 32];
@@ -180,17 +184,24 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             // (the queue slot of an unused place may hold a forward piece sum: read 0 there)
             float gr = (j < d ? res[q * 32 + lane] : 0.f) + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
             gr += (j == bestj) ? extra : 0.f;
-            m[q] = fmaf(b1, m[q], omb1 * gr);
-            v[q] = fmaf(b2, v[q], omb2 * gr * gr);
-            const float den = fmaf(umma::sqrt_approx(v[q]), st.z, eps);
-            const float zn = fmaf(-st.x * m[q], umma::rcp_approx(den), zz);
+            float zn;
+            if (opt == 0) {   // Adam (reading #9)
+                m[q] = fmaf(b1, m[q], omb1 * gr);
+                v[q] = fmaf(b2, v[q], omb2 * gr * gr);
+                const float den = fmaf(umma::sqrt_approx(v[q]), st.z, eps);
+                zn = fmaf(-st.x * m[q], umma::rcp_approx(den), zz);
+            } else if (opt == 1) {   // GD (reading #24): two roundings, as z - lr * g in fp32
+                zn = __fsub_rn(zz, __fmul_rn(lr, gr));
+            } else {                 // sign-GD
+                zn = __fsub_rn(zz, gr > 0.f ? lr : (gr < 0.f ? -lr : 0.f));
+            }
             zsh[j] = zn;
             const float rn = round_half_away_f(zn);
             changed |= rn != round_half_away_f(zz);
             grsh[j] = rn;
         }
         __syncwarp();
-        if (!p.harvest) continue;
+        if (!p.harvest || (p.harvest_final && !final_step)) continue;
         // harvest (Alg. 3 lines 9-10) when round(z) changed: g = B r, box, g != 0, canonical sign
         if (!__any_sync(0xffffffffu, changed)) continue;
         bool ok = true;

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
     const int t_end = harvest ? T + 1 : T;
     for (int t = 1; t <= t_end; ++t) {
         const bool do_fwd = t <= T;
-        const bool do_harv = harvest && t >= 2;
+        const bool do_harv = harvest && (p.harvest_final ? t == T + 1 : t >= 2);
         fence_proxy_async();
         fence_before();
         __syncthreads();  // B1: operands written, pair info visible
@@ -240,7 +240,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
             for (int e = 0; e < 4; ++e) bq[e] = __float_as_uint(__uint_as_float(r4[e]) + 12582912.f);
             return __byte_perm(__byte_perm(bq[0], bq[1], 0x0040), __byte_perm(bq[2], bq[3], 0x0040), 0x5410);
         };
-        const bool row_chg = do_harv && active && (chg[row] | chg[kRows + row]) == 1;
+        // rows whose round(z) changed (every-step harvest), or every row (final-only); never a row whose
+        // iterate left the f16 range of the harvest operand (bit 1, see below)
+        const uint8_t cflag = chg[row] | chg[kRows + row];
+        const bool row_chg = do_harv && active && (p.harvest_final ? (cflag & 2) == 0 : cflag == 1);
         const bool warp_harv = __any_sync(0xffffffffu, row_chg);
         if (do_harv) {
             // ---- harvest test of g = H row (z_{t-1}), this half's columns: box |g| <= u - l and the sign of
@@ -364,13 +367,17 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
         bool ch = (t == 1);
         float lmax = 0.f;   // max |z_new| over this half and its first index (strict >: lowest index wins)
         int lq = 0;
-        auto adam = [&](auto has_extra) {
+        const float lr = p.lr;
+        auto adam = [&](auto has_extra, auto opt) {
+            constexpr int OPT = decltype(opt)::value;   // reading #24: 0 Adam, 1 GD, 2 sign-GD
 #pragma unroll
             for (int c = 0; c < DH / 8; ++c) {
                 uint32_t rg[8], rm[8], rv[8];
                 ld8(tl + L::CG + half * DH + 8 * c, rg);
-                ld8(tl + L::CM + half * DH + 8 * c, rm);
-                ld8(tl + L::CV + half * DH + 8 * c, rv);
+                if constexpr (OPT == 0) {
+                    ld8(tl + L::CM + half * DH + 8 * c, rm);
+                    ld8(tl + L::CV + half * DH + 8 * c, rv);
+                }
                 // current iterate z = Z_hi + Z_lo and r = round(z) (the f16 harvest operand written last step)
                 const uint32_t roff = op_offset(row, half * (DH / 8) + c, kRows);
                 const uint4 rw = *reinterpret_cast<const uint4*>(sm + L::R16 + roff);
@@ -383,8 +390,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                     lo[u] = *reinterpret_cast<const float4*>(sm + L::ZLO + off);
                 }
                 wait8(rg);
-                wait8(rm);
-                wait8(rv);
+                if constexpr (OPT == 0) {
+                    wait8(rm);
+                    wait8(rv);
+                }
                 float rn8[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
@@ -401,12 +410,19 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                     if constexpr (decltype(has_extra)::value) {
                         if (q == kq) g += extra;
                     }
-                    const float mm = fmaf(b1, __uint_as_float(rm[e]), omb1 * g);
-                    const float vv = fmaf(b2, __uint_as_float(rv[e]), omb2 * g * g);
-                    rm[e] = __float_as_uint(mm);
-                    rv[e] = __float_as_uint(vv);
-                    const float den = fmaf(sqrt_approx(vv), st.z, eps);
-                    const float zn = fmaf(-st.x * mm, rcp_approx(den), zz);
+                    float zn;
+                    if constexpr (OPT == 0) {
+                        const float mm = fmaf(b1, __uint_as_float(rm[e]), omb1 * g);
+                        const float vv = fmaf(b2, __uint_as_float(rv[e]), omb2 * g * g);
+                        rm[e] = __float_as_uint(mm);
+                        rv[e] = __float_as_uint(vv);
+                        const float den = fmaf(sqrt_approx(vv), st.z, eps);
+                        zn = fmaf(-st.x * mm, rcp_approx(den), zz);
+                    } else if constexpr (OPT == 1) {
+                        zn = __fsub_rn(zz, __fmul_rn(lr, g));   // two roundings, as z - lr * g in fp32
+                    } else {
+                        zn = __fsub_rn(zz, g > 0.f ? lr : (g < 0.f ? -lr : 0.f));
+                    }
                     const float tn = truncf(zn);
                     const float dn = zn - tn;
                     // round half away from zero; + 0 turns -0 into +0 so equal values have equal f16 bits
@@ -418,8 +434,10 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                     hp[e & 3] = tf32_rna(zn);
                     lp[e & 3] = zn - hp[e & 3];
                 }
-                st8(tl + L::CM + half * DH + 8 * c, rm);
-                st8(tl + L::CV + half * DH + 8 * c, rv);
+                if constexpr (OPT == 0) {
+                    st8(tl + L::CM + half * DH + 8 * c, rm);
+                    st8(tl + L::CV + half * DH + 8 * c, rv);
+                }
                 uint32_t rnew[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -436,10 +454,20 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                 *reinterpret_cast<uint4*>(sm + L::R16 + roff) = make_uint4(rnew[0], rnew[1], rnew[2], rnew[3]);
             }
         };
-        if (__any_sync(0xffffffffu, extra != 0.f))
-            adam(std::integral_constant<bool, true>());
-        else
-            adam(std::integral_constant<bool, false>());
+        using I0 = std::integral_constant<int, 0>;
+        using I1 = std::integral_constant<int, 1>;
+        using I2 = std::integral_constant<int, 2>;
+        const bool any_extra = __any_sync(0xffffffffu, extra != 0.f);
+        if (p.opt == 0) {
+            if (any_extra) adam(std::true_type(), I0());
+            else adam(std::false_type(), I0());
+        } else if (p.opt == 1) {
+            if (any_extra) adam(std::true_type(), I1());
+            else adam(std::false_type(), I1());
+        } else {
+            if (any_extra) adam(std::true_type(), I2());
+            else adam(std::false_type(), I2());
+        }
         st_wait();
         amax[((t & 1) * 2 + half) * kRows + row] = lmax;
         aidx[((t & 1) * 2 + half) * kRows + row] = lq;

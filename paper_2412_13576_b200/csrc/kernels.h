@@ -36,6 +36,9 @@ struct DescentParams {
     const int32_t* hi;            // u (n)
     const int32_t* box;           // u - l (n)
     int harvest;                  // 0: descent only (debug)
+    int opt;                      // line 8's update (reading #24): 0 Adam, 1 GD (z - lr g), 2 sign-GD (z - lr sign g)
+    int harvest_final;            // 1: harvest the final iterate only (reading #25)
+    float lr;                     // step size (GD / sign-GD)
     int8_t* cand;                 // candidate rows, stride n_pad
     int64_t cand_cap;
     unsigned long long* cand_count;

@@ -64,6 +64,7 @@ _SIGS = [
     ("maple_set_descent_kernel", C.c_int, [_P, C.c_int32]),
     ("maple_descent_kernel", C.c_int, [_P]),
     ("maple_set_filter_algorithm", C.c_int, [_P, C.c_int32]),
+    ("maple_set_descent_variant", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
     ("maple_feasible_starts", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, _P,
                                         C.c_int32, _P, _P]),
@@ -218,6 +219,11 @@ class Context:
 
     def set_descent_kernel(self, which: int):
         _check(_lib.maple_set_descent_kernel(self.h, which), self.h)
+
+    def set_descent_variant(self, optimizer: str = "adam", harvest_final: bool = False):
+        """Alg. 3 line 8 update ('adam', 'gd', 'signgd') and final-only harvest (maple_set_descent_variant)."""
+        code = {"adam": 0, "gd": 1, "signgd": 2}[optimizer]
+        _check(_lib.maple_set_descent_variant(self.h, code, int(harvest_final)), self.h)
 
     def set_filter_algorithm(self, which: int):
         """0 auto, 1 tiled, 2 indexed (maple_set_filter_algorithm): same kept set, different pair enumeration."""

@@ -272,3 +272,56 @@ def test_filter_algorithms_identical(gpu_lib, name, N):
     if name == "C1":   # (the other shapes' G1 tests run through the auto = indexed filter)
         ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, ctx.candidates())
         assert nbad == 0 and [tuple(r) for r in out[1].tolist()] == ref
+
+
+@pytest.mark.parametrize("name,kernel", [("C1", TC), ("C1", SIMT), ("C2a", TC), ("C2a", SIMT), ("C3", SIMT)])
+@pytest.mark.parametrize("opt", ["gd", "signgd"])
+def test_descent_variants_iterates(gpu_lib, name, kernel, opt):
+    """Readings #24 (GD, sign-GD): per-start iterates vs the fp64 oracle — every start within 1e-4 at T = 5;
+    at T = 50 no worse than IEEE fp32 arithmetic of the same algorithm (gate G2)."""
+    from synth import config
+    inst = config(name)
+    ctx = _ctx(gpu_lib, inst, kernel)
+    ctx.set_descent_variant(opt)
+    N = 1000 if name != "C3" else 128
+    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
+    Z, _ = ctx.debug_descent(N, 0, N, 5, inst.lr, inst.seed)
+    assert _pass_frac(Z, OX.descend(z0, ctx.B, 5, inst.lr, optimizer=opt)) >= 0.999
+    Z, _ = ctx.debug_descent(N, 0, N, 50, inst.lr, inst.seed)
+    Z64 = OX.descend(z0, ctx.B, 50, inst.lr, optimizer=opt)
+    Z32 = OX.descend(z0.astype(np.float32), ctx.B, 50, inst.lr, optimizer=opt, dtype=np.float32)
+    assert _pass_frac(Z, Z64) >= _pass_frac(Z32, Z64) - 0.01
+
+
+@pytest.mark.parametrize("name,kernel", [("C1", TC), ("C2a", TC), ("C2a", SIMT), ("C2b", TC), ("C3", SIMT)])
+@pytest.mark.parametrize("opt", ["adam", "signgd"])
+def test_final_only_harvest_bit_exact(gpu_lib, name, kernel, opt):
+    """Reading #25: with the final-only harvest the candidate set is exactly the oracle's harvest (B⌈z⌋ in
+    the box, g != 0, canonical) of the GPU's own final iterates, and the post-processing of those candidates
+    is bit-exact (G1)."""
+    from synth import config
+    inst = config(name)
+    ctx = _ctx(gpu_lib, inst, kernel)
+    ctx.set_descent_variant(opt, harvest_final=True)
+    N = 777 if name != "C3" else 96
+    Z, _ = ctx.debug_descent(N, 0, N, inst.steps, inst.lr, inst.seed)
+    ctx.set_debug(True)
+    ds = ctx.extract(N, inst.steps, inst.lr, inst.seed)
+    cand = ctx.candidates()
+    assert _set(cand) == _set(OX.harvest(Z.astype(np.float64), ctx.B, inst.l, inst.u))
+    ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, cand)
+    assert nbad == 0 and [tuple(r) for r in ds.rows().tolist()] == ref
+
+
+def test_variant_c1_sets_within_closed_form(gpu_lib):
+    """Every variant on BASELINE configs[0]: exact rows, ⊑-minimal set inside {e_i - e_j}."""
+    from synth import c1
+    inst = c1()
+    expected = {OG.canonical(g) for g in OG.graver_in_box(inst.A, [-3] * 4, [3] * 4)}
+    for opt in ("gd", "signgd"):
+        for fin in (False, True):
+            ctx = _ctx(gpu_lib, inst)
+            ctx.set_descent_variant(opt, harvest_final=fin)
+            rows = ctx.extract(1024, inst.steps, inst.lr, inst.seed).rows()
+            assert np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
+            assert _set(rows) <= expected

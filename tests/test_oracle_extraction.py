@@ -149,3 +149,54 @@ def test_fp32_mode_runs_same_algorithm():
     Z32 = X.descend(z0.astype(np.float32), B, 5, 0.01, dtype=np.float32)
     assert Z32.dtype == np.float32
     np.testing.assert_allclose(Z32, Z64, rtol=1e-5, atol=1e-5)
+
+
+def test_gd_matches_torch_sgd():
+    """Reading #24, plain GD (a first-order method): z <- z - lr g is torch.optim.SGD without momentum."""
+    torch = pytest.importorskip("torch")
+    B = np.array([[1, -1, 0], [0, 1, -1], [1, 0, 1], [2, -1, 1]], dtype=np.float64)
+    z0 = np.random.default_rng(4).uniform(-2, 2, size=(5, 3))
+    ours = X.descend(z0, B, steps=25, lr=0.05, optimizer="gd")
+    p = torch.tensor(z0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.SGD([p], lr=0.05)
+    for _ in range(25):
+        opt.zero_grad()
+        p.grad = torch.from_numpy(X.subgrad(p.detach().numpy().copy(), B, 0.85, 1.0))
+        opt.step()
+    np.testing.assert_allclose(ours, p.detach().numpy(), rtol=1e-13, atol=1e-14)
+
+
+def test_signgd_moves_each_coordinate_by_lr_against_the_subgradient():
+    """Reading #24, sign-GD: every coordinate moves by exactly lr (or 0 where the subgradient is 0), opposite
+    to the subgradient's sign; at the λ1 = λ2 = 0 limit on B = (1, -1)^T from z = 0.3 the ℓ1 term alone
+    walks z down by lr per step until it crosses 0, then oscillates within lr of 0."""
+    B = np.array([[1, -1, 0], [0, 1, -1], [1, 0, 1], [2, -1, 1]], dtype=np.float64)
+    z0 = np.random.default_rng(5).uniform(-2, 2, size=(64, 3))
+    g = X.subgrad(z0, B, 0.85, 1.0)
+    z1 = X.descend(z0, B, steps=1, lr=0.0625, optimizer="signgd")   # lr = 2^-4: z0 - lr is exact here
+    step = z0 - z1
+    np.testing.assert_array_equal(np.abs(step)[g != 0], 0.0625)
+    np.testing.assert_array_equal(np.sign(step), np.sign(g))
+    traj = []
+    X.descend(np.array([[0.3]]), np.array([[1.0], [-1.0]]), steps=8, lr=0.0625, lam1=0.0, lam2=0.0,
+              optimizer="signgd", trace=traj)
+    zs = [float(t[0, 0]) for t in traj]
+    assert zs[:4] == [0.3 - 0.0625 * k for k in range(1, 5)]
+    assert all(abs(z) <= 0.0625 for z in zs[4:])
+
+
+def test_variant_extractions_on_c1_are_graver():
+    """Readings #24/#25 at BASELINE configs[0]: every optimizer variant and the final-only harvest yield
+    kernel elements in the box (soundness), a ⊑-minimal set inside the closed form {e_i - e_j}, and the
+    final-only pool is exactly the harvest of the final iterates (a subset of the every-step pool)."""
+    inst, B = _c1_problem()
+    expected = {Gv.canonical(g) for g in Gv.graver_in_box(inst.A, [-3] * 4, [3] * 4)}
+    for opt in ("gd", "signgd"):
+        pool, _ = X.extract_pool(B, L.pinv(B), inst.l, inst.u, 512, 200, 0.01, seed=1, optimizer=opt)
+        rows = np.array(sorted(pool))
+        assert len(pool) > 0 and np.all(PP.check_rows(inst.A, inst.l, inst.u, rows))
+        assert PP.minimal_filter(pool) <= expected
+    every, _ = X.extract_pool(B, L.pinv(B), inst.l, inst.u, 256, 100, 0.01, seed=2)
+    final, Z = X.extract_pool(B, L.pinv(B), inst.l, inst.u, 256, 100, 0.01, seed=2, harvest_final=True)
+    assert final <= every
+    assert final == {tuple(int(x) for x in r) for r in X.harvest(Z, B, inst.l, inst.u)}
