@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
     uint8_t* chg = reinterpret_cast<uint8_t*>(aidx + 2 * 2 * kRows);  // [half][row]
     int8_t* hx = reinterpret_cast<int8_t*>(chg + 2 * kRows);           // [half][row]: harvest test, see below
     unsigned long long* slot_sh = reinterpret_cast<unsigned long long*>(hx + 2 * kRows);   // [row]
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + L::MBAR);
-    uint32_t* tbase_sh = reinterpret_cast<uint32_t*>(mbar + 2);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(sm + L::MBAR);   // [0] forward, [1] backward, [2] harvest MMAs
+    uint32_t* tbase_sh = reinterpret_cast<uint32_t*>(mbar + 3);
     float* boxs = reinterpret_cast<float*>(sm + L::BOX);
 
     // ---- setup: TMEM, barriers, B operands (exact small integers) ----
@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
     if (tid == 0) {
         mbar_init(&mbar[0], 1);
         mbar_init(&mbar[1], 1);
+        mbar_init(&mbar[2], 1);
         fence_mbar_init();
     }
     for (int e = tid; e < NP * DP; e += kThreads) {
@@ -165,8 +166,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                 if (j < d && active && p.Z0_out) p.Z0_out[local * d + j] = zacc[q];
                 (&hi[e >> 2].x)[e & 3] = tf32_rna(zz);
                 (&lo[e >> 2].x)[e & 3] = zz - tf32_rna(zz);
-                const float tq = truncf(zz), dq = zz - tq;
-                const float rq = fabsf(dq) >= 0.5f ? tq + copysignf(1.f, dq) : tq;
+                const float rq = round_half_away_f(zz);
                 const uint32_t hb = __half_as_ushort(__float2half_rn(rq));
                 rnew[e >> 1] = (e & 1) ? (rnew[e >> 1] | (hb << 16)) : hb;
                 if (fabsf(zz) > lmax) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
     const bool harvest = p.harvest != 0;
     const int64_t cap = p.cand_cap;
 
-    uint32_t phA = 0, phB = 0;
+    uint32_t phA = 0, phB = 0, phC = 0;
     const int t_end = harvest ? T + 1 : T;
     for (int t = 1; t <= t_end; ++t) {
         const bool do_fwd = t <= T;
@@ -216,19 +216,28 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                 for (int kk = 0; kk < DP / 8; ++kk)
                     mma_tf32(tbase + L::CG, desc(sZLO + kk * 2 * LBO_A, LBO_A, SBO),
                              desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, 1);
+                commit(&mbar[0]);
             }
-            if (do_harv) {
+            if (do_harv) {   // committed separately: it runs while the sign epilogue reads G
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk)
                     mma_f16(tbase + L::CX, desc(sR + kk * 2 * LBO_A, LBO_A, SBO),
                             desc(sB16 + kk * 2 * LBO_N, LBO_N, SBO), ID_HARV, kk > 0);
+                commit(&mbar[2]);
             }
-            commit(&mbar[0]);
         }
-        // one warp polls the mbarrier; the others wait in the CTA barrier without issuing
-        if (warp == 0) mbar_wait(&mbar[0], phA);
-        phA ^= 1;
+        if (do_fwd) {
+#ifndef MAPLE_TC_CTA_WAIT
+            mbar_wait(&mbar[0], phA);
+#else
+            // one warp polls the mbarrier; the others wait in the CTA barrier without issuing
+            if (warp == 0) mbar_wait(&mbar[0], phA);
+#endif
+            phA ^= 1;
+        }
+#ifdef MAPLE_TC_CTA_WAIT
         __syncthreads();
+#endif
         fence_after();
         constexpr int NH = NP / 2;
         constexpr int CW = NH % 16 == 0 ? 16 : 8;   // columns per TMEM load batch (NH is a multiple of 8)
@@ -245,7 +254,36 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
         const uint8_t cflag = chg[row] | chg[kRows + row];
         const bool row_chg = do_harv && active && (p.harvest_final ? (cflag & 2) == 0 : cflag == 1);
         const bool warp_harv = __any_sync(0xffffffffu, row_chg);
+        if (do_fwd) {
+            // ---- S = sign(B z), this half's columns of G -> bf16 backward operand ----
+            // sign via bf16 pairs: rounding to bf16 never flips a sign and has fp32's exponent range
+            const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
+#pragma unroll
+            for (int c0 = 0; c0 < NH; c0 += CW) {
+                uint32_t r[CW];
+                ld8(tl + L::CG + c_lo + c0, &r[0]);
+                if constexpr (CW == 16) ld8(tl + L::CG + c_lo + c0 + 8, &r[8]);
+                wait8(&r[0]);
+                if constexpr (CW == 16) wait8(&r[8]);
+#pragma unroll
+                for (int c = 0; c < CW / 8; ++c) {
+                    uint4 w;
+                    uint32_t* wp = &w.x;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const __nv_bfloat162 h =
+                            __floats2bfloat162_rn(__uint_as_float(r[8 * c + 2 * e]), __uint_as_float(r[8 * c + 2 * e + 1]));
+                        const __nv_bfloat162 sg = __hsub2(__hgt2(h, zero2), __hlt2(h, zero2));
+                        wp[e] = *reinterpret_cast<const uint32_t*>(&sg);
+                    }
+                    *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, (c_lo + c0) / 8 + c, kRows)) = w;
+                }
+            }
+        }
         if (do_harv) {
+            mbar_wait(&mbar[2], phC);   // every warp; the harvest MMA ran during the sign epilogue
+            phC ^= 1;
+            fence_after();
             // ---- harvest test of g = H row (z_{t-1}), this half's columns: box |g| <= u - l and the sign of
             // the first nonzero. hx = 0: fails the box; 1: in the box, all zero here; 2 / 3: first nonzero > 0 / < 0
             int8_t code = 1;
@@ -273,32 +311,6 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                 code = !ok ? 0 : (sgn == 0 ? 1 : (sgn > 0 ? 2 : 3));
             }
             hx[half * kRows + row] = code;
-        }
-        if (do_fwd) {
-            // ---- S = sign(B z), this half's columns of G -> bf16 backward operand ----
-            // sign via bf16 pairs: rounding to bf16 never flips a sign and has fp32's exponent range
-            const __nv_bfloat162 zero2 = __float2bfloat162_rn(0.f);
-#pragma unroll
-            for (int c0 = 0; c0 < NH; c0 += CW) {
-                uint32_t r[CW];
-                ld8(tl + L::CG + c_lo + c0, &r[0]);
-                if constexpr (CW == 16) ld8(tl + L::CG + c_lo + c0 + 8, &r[8]);
-                wait8(&r[0]);
-                if constexpr (CW == 16) wait8(&r[8]);
-#pragma unroll
-                for (int c = 0; c < CW / 8; ++c) {
-                    uint4 w;
-                    uint32_t* wp = &w.x;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const __nv_bfloat162 h =
-                            __floats2bfloat162_rn(__uint_as_float(r[8 * c + 2 * e]), __uint_as_float(r[8 * c + 2 * e + 1]));
-                        const __nv_bfloat162 sg = __hsub2(__hgt2(h, zero2), __hlt2(h, zero2));
-                        wp[e] = *reinterpret_cast<const uint32_t*>(&sg);
-                    }
-                    *reinterpret_cast<uint4*>(sm + L::S16 + op_offset(row, (c_lo + c0) / 8 + c, kRows)) = w;
-                }
-            }
         }
         fence_proxy_async();
         fence_before();
@@ -344,9 +356,15 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
             }
         }
         if (!do_fwd) break;
+#ifndef MAPLE_TC_CTA_WAIT
+        mbar_wait(&mbar[1], phB);
+#else
         if (warp == 0) mbar_wait(&mbar[1], phB);
+#endif
         phB ^= 1;
+#ifdef MAPLE_TC_CTA_WAIT
         __syncthreads();
+#endif
         fence_after();
         // ---- gradient of Eq. 3 + Adam, this thread's coordinate half, 8 coordinates at a time ----
         const int par = (t - 1) & 1;
@@ -423,10 +441,8 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                     } else {
                         zn = __fsub_rn(zz, g > 0.f ? lr : (g < 0.f ? -lr : 0.f));
                     }
-                    const float tn = truncf(zn);
-                    const float dn = zn - tn;
-                    // round half away from zero; + 0 turns -0 into +0 so equal values have equal f16 bits
-                    rn8[e] = (fabsf(dn) >= 0.5f ? tn + copysignf(1.f, dn) : tn) + 0.f;
+                    // round half away from zero; +0 (never -0) so equal values have equal f16 bits
+                    rn8[e] = round_half_away_f(zn);
                     if (fabsf(zn) > lmax) {
                         lmax = fabsf(zn);
                         lq = q;
