@@ -76,6 +76,10 @@ EllSchedule build_ell(const std::vector<std::vector<std::pair<int, int>>>& lists
         while (b < 32 && ((used >> b) & 1u)) ++b;
         return (b < 32 && b < gather_limit) ? b : 0;
     };
+    // Per slot: a maximum matching of the lanes that hold real entries to shared-memory banks (lane L may take
+    // bank b if an entry of its current piece gathers from bank b; Kuhn's augmenting paths, lanes with the
+    // fewest options first), so as many lanes as possible gather conflict-free. A lane left unmatched takes the
+    // entry whose bank is least used in the slot (the gather then costs two wavefronts; keep it at two).
     for (int e = 0;; ++e) {
         bool any = false;
         for (int L = 0; L < 32; ++L) any |= ln[L].pos < mine[L].size();
@@ -83,20 +87,69 @@ EllSchedule build_ell(const std::vector<std::vector<std::pair<int, int>>>& lists
         uint32_t used = 0;
         uint32_t slot[32];
         bool later[32];
-        for (int k = 0; k < 32; ++k) {   // lanes with real entries pick first (rotating priority)
-            const int L = (e + k) & 31;
+        uint32_t opts[32];
+        int order[32], nact = 0;
+        for (int L = 0; L < 32; ++L) {
             Lane& s = ln[L];
             later[L] = s.pos >= mine[L].size() || s.rem.empty();
+            opts[L] = 0;
             if (later[L]) continue;
-            size_t pick = 0;
-            bool got = false;
-            for (size_t c = 0; c < s.rem.size(); ++c)
-                if (!(used & (1u << (s.rem[c].first & 31)))) {
-                    pick = c;
-                    got = true;
-                    break;
+            for (const auto& en : s.rem) opts[L] |= 1u << (en.first & 31);
+            order[nact++] = L;
+        }
+        std::stable_sort(order, order + nact, [&](int a, int b) {
+            const int pa = __builtin_popcount(opts[a]), pb = __builtin_popcount(opts[b]);
+            return pa != pb ? pa < pb : ((a - e) & 31) < ((b - e) & 31);
+        });
+        int bank_of[32], lane_of[32];
+        for (int k = 0; k < 32; ++k) bank_of[k] = lane_of[k] = -1;
+        for (int k = 0; k < nact; ++k) {
+            const int L0 = order[k];
+            uint32_t seen = 0;
+            // iterative DFS for an augmenting path from lane L0
+            struct Fr { int lane; uint32_t left; };
+            Fr st[33];
+            int sp = 0;
+            st[sp++] = {L0, opts[L0]};
+            int path_bank[33];
+            bool found = false;
+            while (sp > 0 && !found) {
+                Fr& fr = st[sp - 1];
+                const uint32_t cand = fr.left & ~seen;
+                if (!cand) { --sp; continue; }
+                const int b = __builtin_ctz(cand);
+                fr.left &= ~(1u << b);
+                seen |= 1u << b;
+                path_bank[sp - 1] = b;
+                if (lane_of[b] < 0) { found = true; break; }
+                st[sp++] = {lane_of[b], opts[lane_of[b]]};
+            }
+            if (found)
+                for (int q = sp - 1; q >= 0; --q) {   // flip the path: lane st[q] takes bank path_bank[q]
+                    const int L = st[q].lane, b = path_bank[q];
+                    bank_of[L] = b;
+                    lane_of[b] = L;
                 }
-            if (!got) ++S.conflicts;
+        }
+        int cnt[32] = {0};
+        for (int L = 0; L < 32; ++L)
+            if (!later[L] && bank_of[L] >= 0) cnt[bank_of[L]]++;
+        for (int k = 0; k < nact; ++k) {
+            const int L = order[k];
+            Lane& s = ln[L];
+            size_t pick = 0;
+            if (bank_of[L] >= 0) {
+                for (size_t c = 0; c < s.rem.size(); ++c)
+                    if ((s.rem[c].first & 31) == bank_of[L]) { pick = c; break; }
+            } else {
+                ++S.conflicts;
+                int best = 1 << 30;
+                for (size_t c = 0; c < s.rem.size(); ++c) {
+                    const int b = s.rem[c].first & 31;
+                    if (cnt[b] < best) { best = cnt[b]; pick = c; }
+                }
+                cnt[s.rem[pick].first & 31]++;
+            }
             const auto ent = s.rem[pick];
             s.rem.erase(s.rem.begin() + (long)pick);
             used |= 1u << (ent.first & 31);
