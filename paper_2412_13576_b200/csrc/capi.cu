@@ -98,7 +98,7 @@ struct maple_ctx {
     HostStage stage_aug, stage_tab;   // pinned upload staging (augmentation inputs, Adam step table)
     int tab_T = -1;                   // the step table on the device was built for (tab_T, tab_lr, betas)
     double tab_lr = 0, tab_b1 = 0, tab_b2 = 0;
-    DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned;   // SIMT schedules of B (sparse_ell.h)
+    DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned, ell_pos_s;   // SIMT schedules of B (sparse_ell.h)
     int ell_conflicts = 0;
     DevBuf AT_ptr, AT_row, AT_val, fb, frows, fX;
     SparseB sb{};
@@ -558,8 +558,33 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         // uneven: C3's longest has 91 nonzeros against 38 per lane); columns stay whole (Adam ownership)
         if (std::max(n, d) > kEllMaxIndex) return MAPLE_ERR_RANGE;
         const int chunk = std::max(4, ((nnz + 31) / 32 + 3) / 4);
-        const EllSchedule F = build_ell(rows, d, chunk);   // PAD gathers < d: z[d] is the SIMT scratch slot
-        const EllSchedule Bk = build_ell(cols, n, 0);
+        // Storage in owner order: coordinate j of z (and of r = round(z)) lives at its backward place q*32 + L
+        // (lane L owns it for Adam), row i of s = sign(Bz) (and of the harvested g) at its forward place; split
+        // rows after the qf*32 places. Adam and the forward stores then touch contiguous, conflict-free words,
+        // and a gather's bank is the owner lane of what it gathers. The lane assignment depends only on the
+        // list lengths, so a first pass fixes the places and the second schedules the remapped gathers.
+        const EllSchedule F0 = build_ell(rows, d, chunk);
+        const EllSchedule B0 = build_ell(cols, n, 0);
+        const int qf0 = std::max(F0.max_pieces, 1), qd0 = std::max(B0.max_pieces, 1);
+        std::vector<int> pz(d, -1), ps(n, -1);
+        for (size_t k = 0; k < B0.owned.size(); ++k)
+            if (B0.owned[k] >= 0) pz[B0.owned[k]] = (int)k;
+        for (size_t k = 0; k < F0.owned.size(); ++k)
+            if (F0.owned[k] >= 0) ps[F0.owned[k]] = (int)k;
+        for (size_t f3 = 0; f3 < F0.fixup.size(); f3 += 3) ps[F0.fixup[f3]] = qf0 * 32 + (int)(f3 / 3);
+        auto remap = [](std::vector<std::vector<std::pair<int, int>>> L, const std::vector<int>& pos) {
+            for (auto& l : L)
+                for (auto& e : l) e.first = pos[e.first];
+            return L;
+        };
+        const EllSchedule F = build_ell(remap(rows, pz), qd0 * 32, chunk);
+        const EllSchedule Bk = build_ell(remap(cols, ps), qf0 * 32 + (int)F0.fixup.size() / 3, 0);
+        if (F.owned != F0.owned || Bk.owned != B0.owned || F.fixup != F0.fixup) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        for (int i = 0; i < n; ++i)
+            if (ps[i] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        for (int j = 0; j < d; ++j)
+            if (pz[j] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        CU(upload(ctx->ell_pos_s, std::vector<int32_t>(ps.begin(), ps.end())));
         std::vector<int32_t> fix = F.fixup, fixpos = F.fixpos;
         if (fix.empty()) fix.push_back(0);
         if (fixpos.empty()) fixpos.push_back(0);
@@ -583,6 +608,7 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         sb.fixpos = ctx->ell_fixpos.as<int32_t>();
         sb.ell_b = ctx->ell_b.as<uint32_t>();
         sb.own_b = ctx->ell_owned.as<int32_t>();
+        sb.pos_s = ctx->ell_pos_s.as<int32_t>();
         ctx->ell_conflicts = F.conflicts + Bk.conflicts;
     }
     CU(upload(ctx->th_off, toff));
@@ -621,7 +647,7 @@ void maple_destroy(maple_ctx* ctx) {
     g_alloc_stream = ctx->stream;
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
-                      &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->AT_ptr, &ctx->AT_row,
+                      &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->sig, &ctx->ffreq, &ctx->fkey, &ctx->fbh, &ctx->fbs, &ctx->fbc, &ctx->flrow, &ctx->flsig, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,

@@ -49,13 +49,15 @@ __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slo
 
 // Forward outputs from the result queue: whole rows directly, split rows summed over their pieces in piece
 // order (fixed; reads other lanes' queue entries, hence the warp barrier).
+// store(place, row, value): whole rows at their forward place q * 32 + lane (contiguous per q, conflict-free),
+// split rows at qf * 32 + f.
 template <typename Store>
 __device__ __forceinline__ void ell_rows(const SparseB& sb, const int* __restrict__ ownf, const int* __restrict__ fix,
                                          const int* __restrict__ fixpos, const float* __restrict__ res, int lane,
                                          Store store) {
     for (int q = 0; q < sb.qf; ++q) {
         const int o = ownf[q * 32 + lane];
-        if (o >= 0) store(o, res[q * 32 + lane]);
+        if (o >= 0) store(q * 32 + lane, o, res[q * 32 + lane]);
     }
     if (sb.nfix == 0) return;
     __syncwarp();
@@ -63,7 +65,7 @@ __device__ __forceinline__ void ell_rows(const SparseB& sb, const int* __restric
         const int o = fix[3 * f], b = fix[3 * f + 1], c = fix[3 * f + 2];
         float acc = 0.f;
         for (int k = 0; k < c; ++k) acc += res[fixpos[b + k]];
-        store(o, acc);
+        store(sb.qf * 32 + f, o, acc);
     }
 }
 
@@ -76,31 +78,31 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     const int n = p.n, d = p.d;
     const SparseB& sb = p.sb;
     const int Lf = sb.Lf, Lb = sb.Lb;
-    // block-shared: forward ELL | backward ELL | row pieces (qf x 32) | coordinates (QD x 32) | fixups
+    // block-shared: forward ELL | backward ELL | row pieces (qf x 32) | coordinates (QD x 32) | fixups | places of s
     uint32_t* ellf = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* ellb = ellf + Lf * 32;
     int* ownf = reinterpret_cast<int*>(ellb + Lb * 32);
     int* ownb = ownf + sb.qf * 32;
     int* fix = ownb + QD * 32;
     int* fixpos = fix + 3 * sb.nfix;
+    int* poss = fixpos + sb.nfixpos;
     for (int k = threadIdx.x; k < Lf * 32; k += blockDim.x) ellf[k] = sb.ell_f[k];
     for (int k = threadIdx.x; k < Lb * 32; k += blockDim.x) ellb[k] = sb.ell_b[k];
     for (int k = threadIdx.x; k < sb.qf * 32; k += blockDim.x) ownf[k] = sb.own_f[k];
-    for (int k = threadIdx.x; k < QD * 32; k += blockDim.x) {   // unused places -> scratch coordinate d (< n)
-        const int j = k < sb.qd * 32 ? sb.own_b[k] : -1;
-        ownb[k] = j >= 0 ? j : p.d;
-    }
+    for (int k = threadIdx.x; k < QD * 32; k += blockDim.x) ownb[k] = k < sb.qd * 32 ? sb.own_b[k] : -1;
     for (int k = threadIdx.x; k < 3 * sb.nfix; k += blockDim.x) fix[k] = sb.fix[k];
     for (int k = threadIdx.x; k < sb.nfixpos; k += blockDim.x) fixpos[k] = sb.fixpos[k];
-    const int shared_words = (Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + 1) & ~1);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) poss[k] = sb.pos_s[k];
+    const int shared_words = (Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1);
     __syncthreads();
 
-    // per warp: z [nx] | gr (r after Adam) [nx] | s (then the g row) [n] | result queue; g0 (n doubles) aliases
-    const int nx = n > d ? n : d;
+    // per warp, in owner order (sparse_ell.h / capi): z [QD*32] | r after Adam [QD*32] | s, then the g row
+    // [qf*32 + nfix] | result queue; g0 (n doubles) aliases the front (per_warp_words >= 2n)
+    const int s_words = sb.qf * 32 + sb.nfix;
     float* zsh = reinterpret_cast<float*>(smem_raw) + shared_words + (size_t)wid * per_warp_words;
-    float* grsh = zsh + nx;
-    float* ssh = grsh + nx;
-    float* res = ssh + n;
+    float* grsh = zsh + QD * 32;
+    float* ssh = grsh + QD * 32;
+    float* res = ssh + s_words;
     double* g0sh = reinterpret_cast<double*>(zsh);   // shared_words and per_warp_words are even
 
     const int64_t local = (int64_t)blockIdx.x * nwarps + wid;
@@ -118,20 +120,20 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     for (int q = 0; q < QD; ++q) {
         m[q] = v[q] = 0.f;
         z0[q] = 0.f;
-        if (jq[q * 32] < d) {
+        const int j = jq[q * 32];
+        if (j >= 0) {
             double acc = 0.0;
-            const double* row = p.Bp + (size_t)jq[q * 32] * n;
+            const double* row = p.Bp + (size_t)j * n;
             for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
-            if (p.Z0_out) p.Z0_out[local * d + jq[q * 32]] = acc;
+            if (p.Z0_out) p.Z0_out[local * d + j] = acc;
             z0[q] = (float)acc;
         }
     }
     __syncwarp();
-    for (int k = lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // padding / scratch entries read zeros
+    for (int k = lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // unused places hold z = 0 forever
     __syncwarp();
 #pragma unroll
-    for (int q = 0; q < QD; ++q)
-        if (jq[q * 32] < d) zsh[jq[q * 32]] = z0[q];
+    for (int q = 0; q < QD; ++q) zsh[q * 32 + lane] = z0[q];
     __syncwarp();
 
     const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2, eps = p.eps;
@@ -140,32 +142,36 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     for (int t = 0; t < p.T; ++t) {
         // forward: s_i = sign((B z)_i)
         ell_run(wf, Lf, zsh, res + lane);
-        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int i, float y) { ssh[i] = fsign(y); });
+        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int pl, int, float y) { ssh[pl] = fsign(y); });
         // lowest-index argmax of |z| (λ2 term, Eq. 3), over this lane's coordinates then the warp
         float best = -1.f;
-        int bestj = 0x7fffffff;
+        int bestj = 0x7fffffff, bestp = 0;
 #pragma unroll
-        for (int q = 0; q < QD; ++q) {   // unused places point at the zero scratch coordinate d (loses ties)
+        for (int q = 0; q < QD; ++q) {   // unused places (j < 0) hold z = 0 and lose every tie
             const int j = jq[q * 32];
-            const float aa = fabsf(zsh[j]);
-            if (aa > best || (aa == best && j < bestj)) {
+            const int jj = j >= 0 ? j : 0x7ffffffe;
+            const float aa = fabsf(zsh[q * 32 + lane]);
+            if (aa > best || (aa == best && jj < bestj)) {
                 best = aa;
-                bestj = j;
+                bestj = jj;
+                bestp = q * 32 + lane;
             }
         }
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
             const float ob = __shfl_xor_sync(0xffffffffu, best, off);
             const int oj = __shfl_xor_sync(0xffffffffu, bestj, off);
+            const int op = __shfl_xor_sync(0xffffffffu, bestp, off);
             if (ob > best || (ob == best && oj < bestj)) {
                 best = ob;
                 bestj = oj;
+                bestp = op;
             }
         }
         // λ2 term (Eq. 3), active while max|z| < 1, on the lowest-index argmax coordinate only
         float extra = 0.f;
         if (best < 1.f) {
-            const float zb = zsh[bestj];
+            const float zb = zsh[bestp];
             extra = -lam2 * fsign(zb) / fmaxf(zb * zb, 1e-8f);
         }
         __syncwarp();
@@ -180,9 +186,10 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
 #pragma unroll
         for (int q = 0; q < QD; ++q) {
             const int j = jq[q * 32];
-            const float zz = zsh[j];
+            const int pl = q * 32 + lane;
+            const float zz = zsh[pl];
             // (the queue slot of an unused place may hold a forward piece sum: read 0 there)
-            float gr = (j < d ? res[q * 32 + lane] : 0.f) + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
+            float gr = (j >= 0 ? res[q * 32 + lane] : 0.f) + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
             gr += (j == bestj) ? extra : 0.f;
             float zn;
             if (opt == 0) {   // Adam (reading #9)
@@ -195,10 +202,10 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             } else {                 // sign-GD
                 zn = __fsub_rn(zz, gr > 0.f ? lr : (gr < 0.f ? -lr : 0.f));
             }
-            zsh[j] = zn;
+            zsh[pl] = zn;
             const float rn = round_half_away_f(zn);
             changed |= rn != round_half_away_f(zz);
-            grsh[j] = rn;
+            grsh[pl] = rn;
         }
         __syncwarp();
         if (!p.harvest || (p.harvest_final && !final_step)) continue;
@@ -206,10 +213,10 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
         if (!__any_sync(0xffffffffu, changed)) continue;
         bool ok = true;
         ell_run(wf, Lf, grsh, res + lane);
-        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int i, float acc) {
+        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int pl, int i, float acc) {
             const int gv = (int)acc;
             ok &= (abs(gv) <= p.box[i]);
-            ssh[i] = (float)gv;   // s is dead until the next forward: reuse it as the g row
+            ssh[pl] = (float)gv;   // s is dead until the next forward: reuse it as the g row (row i at place pl)
         });
         ok = __all_sync(0xffffffffu, ok);
         if (!ok) continue;
@@ -217,7 +224,7 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
         int firstsign = 0;
         for (int i0 = 0; i0 < n && !firstsign; i0 += 32) {
             const int i = i0 + lane;
-            const int gv = i < n ? (int)ssh[i] : 0;
+            const int gv = i < n ? (int)ssh[poss[i]] : 0;
             const unsigned msk = __ballot_sync(0xffffffffu, gv != 0);
             if (msk) firstsign = __shfl_sync(0xffffffffu, gv, __ffs(msk) - 1) > 0 ? 1 : -1;
         }
@@ -227,23 +234,25 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
         slot = __shfl_sync(0xffffffffu, slot, 0);
         if ((int64_t)slot < p.cand_cap) {
             int8_t* dst = p.cand + (size_t)slot * p.n_pad;
-            for (int i = lane; i < p.n_pad; i += 32) dst[i] = (i < n) ? (int8_t)(firstsign * (int)ssh[i]) : (int8_t)0;
+            for (int i = lane; i < p.n_pad; i += 32) dst[i] = (i < n) ? (int8_t)(firstsign * (int)ssh[poss[i]]) : (int8_t)0;
         }
         __syncwarp();
     }
     if (p.Z_out) {
 #pragma unroll
         for (int q = 0; q < QD; ++q)
-            if (jq[q * 32] < d) p.Z_out[local * d + jq[q * 32]] = zsh[jq[q * 32]];
+            if (jq[q * 32] >= 0) p.Z_out[local * d + jq[q * 32]] = zsh[q * 32 + lane];
     }
 }
 
 template <int QD>
 cudaError_t launch_qd(const DescentParams& p, cudaStream_t s) {
     const SparseB& sb = p.sb;
-    const int n = p.n, d = p.d, nx = n > d ? n : d;
-    const int per_warp_words = (2 * nx + n + 32 * std::max(sb.qf, QD) + 1) & ~1;
-    const size_t shared_bytes = ((size_t)(sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + 1) & ~1)) * 4;
+    const int n = p.n;
+    const int per_warp_words =
+        (std::max(2 * QD * 32 + sb.qf * 32 + sb.nfix + 32 * std::max(sb.qf, QD), 2 * n) + 1) & ~1;
+    const size_t shared_bytes =
+        ((size_t)(sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1)) * 4;
     int dev = 0, smem_sm = 0, smem_blk = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);

@@ -101,7 +101,7 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned lo
 }
 
 // (C1)-(C3) + filter encoding, one thread per row. The block stages its rows in shared memory (coalesced
-// 16-byte loads, padded stride n_pad + 16); A (CSR), u - l and the thermometer offsets sit in shared memory.
+// 16-byte loads, padded stride n_pad + 4); A (CSR), u - l and the thermometer offsets sit in shared memory.
 constexpr int kCheckThreads = 128;
 __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t* __restrict__ rows,
                                                                    const unsigned long long* dcount, int64_t cap,
@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
     int32_t* soff = sbox + cp.n;
     int32_t* swc0 = soff + cp.n;
     int32_t* swc1 = swc0 + fw.Wh;
-    const int stride = cp.n_pad + 16;
+    // row stride n_pad + 4 bytes: an odd number of 4-byte words, so the 32 threads' reads of the same byte
+    // column of their rows fall in 32 different banks (n_pad + 16 put them in two)
+    const int stride = cp.n_pad + 4;
     int8_t* srow = reinterpret_cast<int8_t*>(sh + (((cp.m + 1 + 2 * cp.nnz + 2 * cp.n + 2 * fw.Wh) + 3) & ~3));
     for (int i = threadIdx.x; i <= cp.m; i += blockDim.x) srp[i] = cp.A_rowptr[i];
     for (int i = threadIdx.x; i < cp.nnz; i += blockDim.x) {
@@ -139,7 +141,14 @@ __global__ void __launch_bounds__(kCheckThreads) check_codes_kernel(const int8_t
         const int64_t nr = min((int64_t)kCheckThreads, count - r0);
         const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r0 * cp.n_pad);
         for (int e = threadIdx.x; e < nr * nw; e += kCheckThreads)
-            *reinterpret_cast<int4*>(srow + (e / nw) * stride + (e % nw) * 16) = src[e];
+        {
+            const int4 v = src[e];
+            uint32_t* dst = reinterpret_cast<uint32_t*>(srow + (e / nw) * stride + (e % nw) * 16);
+            dst[0] = (uint32_t)v.x;
+            dst[1] = (uint32_t)v.y;
+            dst[2] = (uint32_t)v.z;
+            dst[3] = (uint32_t)v.w;
+        }
         __syncthreads();
         if (threadIdx.x >= nr) continue;
         const int8_t* g = srow + threadIdx.x * stride;
@@ -753,7 +762,7 @@ cudaError_t launch_check_codes(const int8_t* rows, const unsigned long long* dco
                                FilterWork& fw, int encode, uint8_t* flags, unsigned long long* n_bad, cudaStream_t s) {
     if (cap <= 0) return cudaSuccess;
     const size_t smem = (size_t)(((cp.m + 1 + 2 * cp.nnz + 2 * cp.n + 2 * fw.Wh) + 3) & ~3) * 4 +
-                        (size_t)kCheckThreads * (cp.n_pad + 16);
+                        (size_t)kCheckThreads * (cp.n_pad + 4);
     if (smem > 200 * 1024) return cudaErrorInvalidValue;
     cudaError_t e = cudaFuncSetAttribute(check_codes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

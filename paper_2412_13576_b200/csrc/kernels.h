@@ -11,12 +11,15 @@ struct SparseB {   // lane-major ELL schedules of B (sparse_ell.h), built once p
     int nnz;                      // nonzeros of B
     int Lf, qf, nfix, nfixpos;    // forward (rows of B): slots, pieces per lane, split rows, their pieces
     int Lb, qd;                   // backward (columns of B): slots, coordinates per lane (whole columns)
-    const uint32_t* ell_f;        // Lf * 32 words, gather z / r (size max(n, d))
+    const uint32_t* ell_f;        // Lf * 32 words, gather z / r (places qd * 32, owner order)
     const int32_t* own_f;         // qf * 32: row of each piece, -1 for pieces of split rows / unused
     const int32_t* fix;           // nfix triples (row, first, count) into fixpos
     const int32_t* fixpos;        // queue positions q * 32 + lane of the split rows' pieces
-    const uint32_t* ell_b;        // Lb * 32 words, gather s (size n)
+    const uint32_t* ell_b;        // Lb * 32 words, gather s (places qf * 32 + nfix)
     const int32_t* own_b;         // qd * 32: coordinate owned by lane L in place q, or -1
+    const int32_t* pos_s;         // n: place of row i in s (forward place q * 32 + L; split rows qf * 32 + f)
+    // z and r live in owner order: coordinate own_b[k] at place k (qd * 32 places); the forward words gather
+    // places, not coordinates
 };
 
 struct DescentParams {
