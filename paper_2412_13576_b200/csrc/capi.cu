@@ -98,7 +98,7 @@ struct maple_ctx {
     HostStage stage_aug, stage_tab;   // pinned upload staging (augmentation inputs, Adam step table)
     int tab_T = -1;                   // the step table on the device was built for (tab_T, tab_lr, betas)
     double tab_lr = 0, tab_b1 = 0, tab_b2 = 0;
-    DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned, ell_pos_s;   // SIMT schedules of B (sparse_ell.h)
+    DevBuf ell_f, ell_own_f, ell_fix, ell_fixpos, ell_b, ell_owned, ell_pos_s, ell_pos_z;   // SIMT schedules of B (sparse_ell.h)
     int ell_conflicts = 0;
     DevBuf AT_ptr, AT_row, AT_val, fb, frows, fX;
     SparseB sb{};
@@ -585,6 +585,7 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         for (int j = 0; j < d; ++j)
             if (pz[j] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
         CU(upload(ctx->ell_pos_s, std::vector<int32_t>(ps.begin(), ps.end())));
+        CU(upload(ctx->ell_pos_z, std::vector<int32_t>(pz.begin(), pz.end())));
         std::vector<int32_t> fix = F.fixup, fixpos = F.fixpos;
         if (fix.empty()) fix.push_back(0);
         if (fixpos.empty()) fixpos.push_back(0);
@@ -609,6 +610,7 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
         sb.ell_b = ctx->ell_b.as<uint32_t>();
         sb.own_b = ctx->ell_owned.as<int32_t>();
         sb.pos_s = ctx->ell_pos_s.as<int32_t>();
+        sb.pos_z = ctx->ell_pos_z.as<int32_t>();
         ctx->ell_conflicts = F.conflicts + Bk.conflicts;
     }
     CU(upload(ctx->th_off, toff));
@@ -647,7 +649,7 @@ void maple_destroy(maple_ctx* ctx) {
     g_alloc_stream = ctx->stream;
     DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
-                      &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->AT_ptr, &ctx->AT_row,
+                      &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->ell_pos_z, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->sig, &ctx->ffreq, &ctx->fkey, &ctx->fbh, &ctx->fbs, &ctx->fbc, &ctx->flrow, &ctx->flsig, &ctx->l1,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,

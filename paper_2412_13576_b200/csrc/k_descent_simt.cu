@@ -86,6 +86,55 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     int* fix = ownb + QD * 32;
     int* fixpos = fix + 3 * sb.nfix;
     int* poss = fixpos + sb.nfixpos;
+    // (at least one row of B+ in fp64: the start computation stages B+ here before the schedules are loaded)
+    const int shared_words = max((Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1), 2 * n);
+
+    // per warp, in owner order (sparse_ell.h / capi): z [QD*32] | r after Adam [QD*32] | s, then the g row
+    // [qf*32 + nfix] | result queue; during the start computation g0 (n doubles) sits behind z
+    // (per_warp_words >= QD*32 + 2n)
+    const int s_words = sb.qf * 32 + sb.nfix;
+    float* zsh = reinterpret_cast<float*>(smem_raw) + shared_words + (size_t)wid * per_warp_words;
+    float* grsh = zsh + QD * 32;
+    float* ssh = grsh + QD * 32;
+    float* res = ssh + s_words;
+    double* g0sh = reinterpret_cast<double*>(grsh);   // shared_words, per_warp_words and QD*32 are even
+
+    const int64_t local = (int64_t)blockIdx.x * nwarps + wid;
+    const bool active = local < p.count;
+    const int64_t gi = p.begin + local;
+
+    // ---- start (Alg. 3 lines 4-5): g0 in fp64 (counter RNG), z0 = B+ g0 in fp64 ----
+    // The block streams B+ once through the (not yet loaded) schedule area, a few rows at a time, and every
+    // warp takes the dot products of its own start with them: B+ is read from L2 once per block instead of
+    // once per start (C3: 672 KB per start before). Each dot product: lanes stride k, fixed-order reduction.
+    for (int k = lane; k < QD * 32; k += 32) zsh[k] = 0.f;   // unused places hold z = 0 forever
+    if (active)
+        for (int k = lane; k < n; k += 32) g0sh[k] = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
+    __syncwarp();
+    {
+        double* stage = reinterpret_cast<double*>(smem_raw);
+        const int R = max(1, (shared_words / 2) / n);   // B+ rows per chunk (shared_words is even)
+        for (int j0 = 0; j0 < d; j0 += R) {
+            const int rows = min(R, d - j0);
+            __syncthreads();
+            for (int e = threadIdx.x; e < rows * n; e += blockDim.x) stage[e] = p.Bp[(size_t)j0 * n + e];
+            __syncthreads();
+            if (!active) continue;
+            for (int r = 0; r < rows; ++r) {
+                const double* br = stage + (size_t)r * n;
+                double acc = 0.0;
+                for (int k = lane; k < n; k += 32) acc = fma(br[k], g0sh[k], acc);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                if (lane == 0) {
+                    const int j = j0 + r;
+                    zsh[sb.pos_z[j]] = (float)acc;
+                    if (p.Z0_out) p.Z0_out[local * d + j] = acc;
+                }
+            }
+        }
+        __syncthreads();
+    }
     for (int k = threadIdx.x; k < Lf * 32; k += blockDim.x) ellf[k] = sb.ell_f[k];
     for (int k = threadIdx.x; k < Lb * 32; k += blockDim.x) ellb[k] = sb.ell_b[k];
     for (int k = threadIdx.x; k < sb.qf * 32; k += blockDim.x) ownf[k] = sb.own_f[k];
@@ -93,48 +142,16 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     for (int k = threadIdx.x; k < 3 * sb.nfix; k += blockDim.x) fix[k] = sb.fix[k];
     for (int k = threadIdx.x; k < sb.nfixpos; k += blockDim.x) fixpos[k] = sb.fixpos[k];
     for (int k = threadIdx.x; k < n; k += blockDim.x) poss[k] = sb.pos_s[k];
-    const int shared_words = (Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1);
     __syncthreads();
-
-    // per warp, in owner order (sparse_ell.h / capi): z [QD*32] | r after Adam [QD*32] | s, then the g row
-    // [qf*32 + nfix] | result queue; g0 (n doubles) aliases the front (per_warp_words >= 2n)
-    const int s_words = sb.qf * 32 + sb.nfix;
-    float* zsh = reinterpret_cast<float*>(smem_raw) + shared_words + (size_t)wid * per_warp_words;
-    float* grsh = zsh + QD * 32;
-    float* ssh = grsh + QD * 32;
-    float* res = ssh + s_words;
-    double* g0sh = reinterpret_cast<double*>(zsh);   // shared_words and per_warp_words are even
-
-    const int64_t local = (int64_t)blockIdx.x * nwarps + wid;
-    if (local >= p.count) return;
-    const int64_t gi = p.begin + local;
+    if (!active) return;
+    for (int k = QD * 32 + lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // g0 is dead: clear r, s, queue
+    __syncwarp();
     const int* jq = ownb + lane;   // jq[q * 32]: this lane's q-th coordinate (shared table, conflict-free)
     const uint32_t* wf = ellf + lane;
     const uint32_t* wb = ellb + lane;
-
-    // ---- start (Alg. 3 lines 4-5): g0 in fp64, z0 = B+ g0 ----
-    for (int k = lane; k < n; k += 32) g0sh[k] = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
-    __syncwarp();
-    float z0[QD], m[QD], v[QD];
+    float m[QD], v[QD];
 #pragma unroll
-    for (int q = 0; q < QD; ++q) {
-        m[q] = v[q] = 0.f;
-        z0[q] = 0.f;
-        const int j = jq[q * 32];
-        if (j >= 0) {
-            double acc = 0.0;
-            const double* row = p.Bp + (size_t)j * n;
-            for (int k = 0; k < n; ++k) acc = fma(row[k], g0sh[k], acc);
-            if (p.Z0_out) p.Z0_out[local * d + j] = acc;
-            z0[q] = (float)acc;
-        }
-    }
-    __syncwarp();
-    for (int k = lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // unused places hold z = 0 forever
-    __syncwarp();
-#pragma unroll
-    for (int q = 0; q < QD; ++q) zsh[q * 32 + lane] = z0[q];
-    __syncwarp();
+    for (int q = 0; q < QD; ++q) m[q] = v[q] = 0.f;
 
     const float b1 = p.beta1, b2 = p.beta2, omb1 = p.omb1, omb2 = p.omb2, lam1 = p.lam1, lam2 = p.lam2, eps = p.eps;
     const float lr = p.lr;
@@ -250,9 +267,9 @@ cudaError_t launch_qd(const DescentParams& p, cudaStream_t s) {
     const SparseB& sb = p.sb;
     const int n = p.n;
     const int per_warp_words =
-        (std::max(2 * QD * 32 + sb.qf * 32 + sb.nfix + 32 * std::max(sb.qf, QD), 2 * n) + 1) & ~1;
+        (std::max(2 * QD * 32 + sb.qf * 32 + sb.nfix + 32 * std::max(sb.qf, QD), QD * 32 + 2 * n) + 1) & ~1;
     const size_t shared_bytes =
-        ((size_t)(sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1)) * 4;
+        (size_t)std::max((sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1), 2 * n) * 4;
     int dev = 0, smem_sm = 0, smem_blk = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);

@@ -18,6 +18,7 @@ struct SparseB {   // lane-major ELL schedules of B (sparse_ell.h), built once p
     const uint32_t* ell_b;        // Lb * 32 words, gather s (places qf * 32 + nfix)
     const int32_t* own_b;         // qd * 32: coordinate owned by lane L in place q, or -1
     const int32_t* pos_s;         // n: place of row i in s (forward place q * 32 + L; split rows qf * 32 + f)
+    const int32_t* pos_z;         // d: place of coordinate j in z (its backward place q * 32 + L)
     // z and r live in owner order: coordinate own_b[k] at place k (qd * 32 places); the forward words gather
     // places, not coordinates
 };

@@ -125,3 +125,39 @@ def test_c4_full_batch_properties(gpu_lib):
     for t in (0, 499, 999):
         x1, f1, _, _ = ctx.augment(ds, Qs[t], cs[t], 0.0, bs[t], X0s[t])
         assert xb[t].tolist() == x1.tolist() and fb[t] == f1
+
+
+def test_c3_large_set_properties(gpu_lib):
+    """C3 (n = 300) with a direction set large enough for the 1,024-thread, unstaged augmentation path
+    (|D| > 16,384, slot-major ELL read from global memory with the early exit at the first blocked coordinate):
+    every incumbent's result is exact and locally optimal over D (Alg. 2's stopping rule), checked on the host
+    in exact integers, and the best is the lexicographic argmin over the incumbents (reading #19)."""
+    from synth import c3, feasible_points
+    inst = c3()
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    ds = ctx.extract(16384, inst.steps, inst.lr, inst.seed)
+    S = ds.rows().astype(np.int64)
+    assert 2 * len(S) > 16384
+    D = np.concatenate([S, -S])
+    X0 = feasible_points(inst, 6, seed=5)
+    Qi, ci = np.asarray(inst.Q, np.int64), np.asarray(inst.c, np.int64)
+    l, u = inst.l.astype(np.int64), inst.u.astype(np.int64)
+    finals = []
+    for x0 in X0:
+        xb, fb, st, it = ctx.augment(ds, inst.Q, inst.c, inst.c0, inst.b, x0[None, :])
+        x = xb.astype(np.int64)
+        assert np.all(inst.A @ x == inst.b) and np.all(x >= l) and np.all(x <= u)
+        two_f = int(x @ Qi @ x + 2 * ci @ x + 2 * inst.c0)
+        assert 2 * fb == two_f
+        assert two_f <= int(x0 @ Qi @ x0 + 2 * ci @ x0 + 2 * inst.c0)
+        with np.errstate(divide="ignore"):
+            up = np.where(D > 0, (u - x)[None, :] // np.where(D > 0, D, 1), np.iinfo(np.int64).max)
+            dn = np.where(D < 0, (x - l)[None, :] // np.where(D < 0, -D, 1), np.iinfo(np.int64).max)
+        lam_max = np.minimum(up.min(axis=1), dn.min(axis=1))
+        lin, quad = D @ (Qi @ x + ci), np.einsum("ki,ij,kj->k", D, Qi, D)
+        for lam in range(1, int(lam_max.max(initial=0)) + 1):
+            ok = lam <= lam_max
+            assert np.all(2 * lam * lin[ok] + lam * lam * quad[ok] >= 0), lam
+        finals.append((two_f, x.tolist()))
+    xb, fb, _, _ = ctx.augment(ds, inst.Q, inst.c, inst.c0, inst.b, X0)
+    assert (2 * fb, xb.tolist()) == min(finals)
