@@ -182,6 +182,8 @@ int read_counters(maple_ctx* ctx, unsigned long long* h) {
 // Size the candidate buffer, the hash set (pool + table) and the per-row work buffers, then reset the set.
 int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
     const int np = ctx->n_pad;
+    // the hash set references rows by 31-bit indices (k_post.cu dedupe_kernel)
+    if (cand_cap >= (int64_t(1) << 31) || pool_cap >= (int64_t(1) << 31)) return MAPLE_ERR_CAPACITY;
     if (cand_cap > ctx->cand_cap) {
         ctx->cand.release();
         CU(ctx->cand.ensure((size_t)cand_cap * np));
@@ -194,7 +196,7 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
         ctx->idx.release();
         CU(ctx->pool.ensure((size_t)pool_cap * np));
         CU(ctx->keys.ensure(slots * 8));
-        CU(ctx->idx.ensure(slots * 4));
+        CU(ctx->idx.ensure((size_t)pool_cap * 8));   // the hash set's newslot array (int64 per pool row)
         ctx->table_slots = slots;
         ctx->pool_cap = pool_cap;
         const int64_t K = pool_cap;
@@ -221,13 +223,13 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
         CU(ctx->fbc.ensure(nbins * 4 + 4));   // + the undecided-row counter
     }
     CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
-    CU(cudaMemsetAsync(ctx->idx.p, 0xFF, ctx->table_slots * 4, ctx->stream));
+    CU(cudaMemsetAsync(ctx->idx.p, 0xFF, (size_t)ctx->pool_cap * 8, ctx->stream));
     CU(cudaMemsetAsync(ctx->counters.p, 0, sizeof(unsigned long long) * C_N, ctx->stream));
     return MAPLE_OK;
 }
 
 HashSet hashset(maple_ctx* ctx) {
-    return HashSet{ctx->keys.as<unsigned long long>(), ctx->idx.as<int32_t>(), ctx->table_slots - 1,
+    return HashSet{ctx->keys.as<unsigned long long>(), ctx->idx.as<int64_t>(), ctx->table_slots - 1,
                    ctx->pool.as<int8_t>(), ctx->pool_cap, counters(ctx) + C_POOL,
                    reinterpret_cast<int*>(counters(ctx) + C_OVF), counters(ctx) + C_MAXC};
 }
@@ -904,15 +906,18 @@ int maple_dirset_copy_device(const maple_dirset* ds, int8_t* dst) {
 
 void maple_dirset_free(maple_dirset* ds) {
     if (!ds) return;
-    // wait for the producing work, then stream-ordered frees back to the pool
+    // wait for the producing work (the set's own event; augmentation, which builds D, synchronises its stream
+    // before returning), then frees back to the pool on the per-thread stream: idle, so the blocks are
+    // reusable at once by the next stream-ordered allocation on any stream, and no legacy-stream barrier
+    // against the context's stream is inserted
     if (ds->ready) {
         cudaEventSynchronize(ds->ready);
         cudaEventDestroy(ds->ready);
     }
-    if (ds->rows) cudaFreeAsync(ds->rows, 0);
-    if (ds->D) cudaFreeAsync(ds->D, 0);
-    if (ds->D_nnz) cudaFreeAsync(ds->D_nnz, 0);
-    if (ds->D_words) cudaFreeAsync(ds->D_words, 0);
+    if (ds->rows) cudaFreeAsync(ds->rows, cudaStreamPerThread);
+    if (ds->D) cudaFreeAsync(ds->D, cudaStreamPerThread);
+    if (ds->D_nnz) cudaFreeAsync(ds->D_nnz, cudaStreamPerThread);
+    if (ds->D_words) cudaFreeAsync(ds->D_words, cudaStreamPerThread);
     delete ds;
 }
 

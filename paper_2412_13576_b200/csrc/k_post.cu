@@ -49,6 +49,11 @@ __device__ __forceinline__ bool rows_equal(const int4* a, const int4* b, int nw)
     return true;
 }
 
+// Slot word: (32-bit hash, never 0) << 32 | ref. ref with bit 31 set = pool index of a finished row; bit 31
+// clear = index of the inserting row in THIS launch's input (rows written by earlier kernels, so a thread that
+// hits the key compares against them without waiting for any write of this launch: no fence, no publication
+// spin). The winner of a slot takes a pool index (warp-aggregated) and records the slot; finish_dedupe_kernel
+// then copies the new rows into the pool and rewrites their slots to pool references.
 __global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned long long* dcount, int64_t cap,
                               int row_stride, int n_pad, HashSet hs) {
     const int nw = n_pad / 16;
@@ -58,15 +63,14 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned lo
          r += (int64_t)gridDim.x * blockDim.x) {
         const int4* src = reinterpret_cast<const int4*>(rows + (size_t)r * row_stride);
         const uint64_t h = row_hash(src, nw);
-        const unsigned long long key = (unsigned long long)(h | 1ULL);
+        const unsigned long long tag = ((h >> 32) | 1ULL) << 32;
         uint64_t pos = mix64(h ^ 0x9E3779B97F4A7C15ULL) & hs.mask;
         for (uint64_t probe = 0; probe <= hs.mask; ++probe) {
             unsigned long long cur = *reinterpret_cast<volatile unsigned long long*>(&hs.keys[pos]);
             if (cur == 0ULL) {
-                cur = atomicCAS(&hs.keys[pos], 0ULL, key);
-                if (cur == 0ULL) {  // we own the slot: publish a new unique row
-                    // opportunistic warp aggregation of the pool-index allocation (one atomic per group of
-                    // lanes that reach this point together instead of one per new row)
+                cur = atomicCAS(&hs.keys[pos], 0ULL, tag | (unsigned long long)r);
+                if (cur == 0ULL) {  // we own the slot: a new unique row
+                    // opportunistic warp aggregation of the pool-index allocation
                     const unsigned am = __activemask();
                     const int lane = threadIdx.x & 31;
                     const int leader = __ffs(am) - 1;
@@ -74,29 +78,39 @@ __global__ void dedupe_kernel(const int8_t* __restrict__ rows, const unsigned lo
                     if (lane == leader) base = atomicAdd(hs.pool_count, (unsigned long long)__popc(am));
                     base = __shfl_sync(am, base, leader);
                     const unsigned long long idx = base + __popc(am & ((1u << lane) - 1u));
-                    if ((int64_t)idx >= hs.pool_cap) {
-                        atomicExch(hs.overflow, 1);
-                        atomicExch(&hs.idx[pos], -2);
-                        break;
-                    }
-                    int4* dst = reinterpret_cast<int4*>(hs.pool + (size_t)idx * n_pad);
-                    for (int i = 0; i < nw; ++i) dst[i] = src[i];
-                    __threadfence();
-                    atomicExch(&hs.idx[pos], (int)idx);
+                    if ((int64_t)idx >= hs.pool_cap)
+                        atomicExch(hs.overflow, 1);   // the caller grows the pool and redoes the extraction
+                    else
+                        hs.newslot[idx] = (int64_t)pos;
                     break;
                 }
             }
-            if (cur == key) {  // same key: wait for publication, then compare the full row
-                int idx;
-                while ((idx = *reinterpret_cast<volatile int*>(&hs.idx[pos])) == -1) {
-                }
-                if (idx == -2) break;  // overflowed insert; reported via hs.overflow
-                __threadfence();
-                const int4* other = reinterpret_cast<const int4*>(hs.pool + (size_t)idx * n_pad);
+            if ((cur & 0xFFFFFFFF00000000ULL) == tag) {  // same hash: compare the full rows
+                const uint32_t ref = (uint32_t)cur;
+                const int4* other = (ref & 0x80000000u)
+                                        ? reinterpret_cast<const int4*>(hs.pool + (size_t)(ref & 0x7FFFFFFFu) * n_pad)
+                                        : reinterpret_cast<const int4*>(rows + (size_t)ref * row_stride);
                 if (rows_equal(src, other, nw)) break;  // duplicate
             }
             pos = (pos + 1) & hs.mask;
         }
+    }
+}
+
+// copy the rows inserted by the last dedupe launch into the pool and turn their slots into pool references
+__global__ void finish_dedupe_kernel(const int8_t* __restrict__ rows, int row_stride, int n_pad, HashSet hs) {
+    const int nw = n_pad / 16;
+    const int64_t count = min((int64_t)*hs.pool_count, hs.pool_cap);
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < count; p += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t pos = hs.newslot[p];
+        if (pos < 0) continue;
+        const unsigned long long cur = hs.keys[pos];
+        const uint32_t ref = (uint32_t)cur;
+        const int4* src = reinterpret_cast<const int4*>(rows + (size_t)ref * row_stride);
+        int4* dst = reinterpret_cast<int4*>(hs.pool + (size_t)p * n_pad);
+        for (int i = 0; i < nw; ++i) dst[i] = src[i];
+        hs.keys[pos] = (cur & 0xFFFFFFFF00000000ULL) | 0x80000000ULL | (unsigned long long)p;
+        hs.newslot[p] = -1;
     }
 }
 
@@ -755,6 +769,7 @@ cudaError_t launch_dedupe(const int8_t* rows, const unsigned long long* dcount, 
                           int n_pad, const HashSet& hs, cudaStream_t s) {
     if (cap <= 0) return cudaSuccess;
     dedupe_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(rows, dcount, cap, row_stride, n_pad, hs);
+    finish_dedupe_kernel<<<grid_for(hs.pool_cap, 256, 148 * 4), 256, 0, s>>>(rows, row_stride, n_pad, hs);
     return cudaGetLastError();
 }
 

@@ -62,8 +62,8 @@ cudaError_t umma_selftest(const float* A1, const float* B1, float* D1, const flo
                           cudaStream_t s);
 
 struct HashSet {
-    unsigned long long* keys;     // 0 = empty
-    int32_t* idx;                 // row index in pool, -1 = not yet published
+    unsigned long long* keys;     // 0 = empty; else (32-bit hash | 1) << 32 | ref (k_post.cu dedupe_kernel)
+    int64_t* newslot;             // per pool index: table slot of a row inserted by the running launch, else -1
     uint64_t mask;                // slots - 1
     int8_t* pool;                 // unique rows, stride n_pad
     int64_t pool_cap;
@@ -72,7 +72,8 @@ struct HashSet {
     unsigned long long* max_count;  // running max of the input counts (detects candidate-buffer overflow)
 };
 
-// Insert min(*dcount, cap) rows (stride row_stride) into the set; new unique rows are appended to the pool.
+// Insert min(*dcount, cap) rows (stride row_stride) into the set; new unique rows are appended to the pool
+// (two launches: the insert and the copy of the new rows). Row indices must be < 2^31.
 cudaError_t launch_dedupe(const int8_t* rows, const unsigned long long* dcount, int64_t cap, int row_stride,
                           int n_pad, const HashSet& hs, cudaStream_t s);
 
