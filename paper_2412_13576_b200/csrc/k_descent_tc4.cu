@@ -113,14 +113,14 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc4_kernel(const DescentP
             g0s[row * (L::KC + 1) + kk] = g;
         }
         __syncthreads();
+        // k outer, coordinates inner: DQ independent fp64 chains per k (the per-coordinate sum stays k-ascending)
+        const int kend = min(L::KC, n - k0);
+        const double* bq = p.Bp + (size_t)(part * DQ) * n + k0;
+        for (int kk = 0; kk < kend; ++kk) {
+            const double g = g0s[row * (L::KC + 1) + kk];
 #pragma unroll
-        for (int q = 0; q < DQ; ++q) {
-            const int j = part * DQ + q;
-            if (j < d) {
-                const double* bp = p.Bp + (size_t)j * n;
-                const int kend = min(L::KC, n - k0);
-                for (int kk = 0; kk < kend; ++kk) zacc[q] = fma(bp[k0 + kk], g0s[row * (L::KC + 1) + kk], zacc[q]);
-            }
+            for (int q = 0; q < DQ; ++q)
+                if (part * DQ + q < d) zacc[q] = fma(bq[(size_t)q * n + kk], g, zacc[q]);
         }
         __syncthreads();
     }
