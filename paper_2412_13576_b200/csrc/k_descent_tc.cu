@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
             int8_t code = 1;
             if (warp_harv) {
                 bool ok = true;
-                int sgn = 0;
+                uint32_t fw = 0u;   // the first nonzero packed word of this half (branch-free select)
 #pragma unroll
                 for (int c0 = 0; c0 < NH; c0 += CW) {
                     uint32_t r[CW];
@@ -305,9 +305,11 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                         ok &= fabsf(__uint_as_float(r[4 * q + 2])) <= bx.z;
                         ok &= fabsf(__uint_as_float(r[4 * q + 3])) <= bx.w;
                         const uint32_t w = pack4(&r[4 * q]);
-                        if (sgn == 0 && w != 0u) sgn = ((int8_t)(w >> (8 * ((__ffs(w) - 1) >> 3)))) > 0 ? 1 : -1;
+                        fw = fw ? fw : w;
                     }
                 }
+                // sign of the first nonzero byte of the first nonzero word
+                const int sgn = fw ? (((int8_t)(fw >> (8 * ((__ffs(fw) - 1) >> 3)))) > 0 ? 1 : -1) : 0;
                 code = !ok ? 0 : (sgn == 0 ? 1 : (sgn > 0 ? 2 : 3));
             }
             hx[half * kRows + row] = code;
