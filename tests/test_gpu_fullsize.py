@@ -133,3 +133,51 @@ def test_c3_directions_vs_oracle(gpu_lib):
     ref, _ = OP.postprocess(inst.A, inst.l, inst.u, np.array(sorted(pool), dtype=np.int64).reshape(-1, inst.n))
     G, R = _set(rows), set(ref)
     assert len(G & R) >= 0.9 * len(G | R)
+
+
+def test_c3_full_size_bench_configuration(gpu_lib):
+    """BASELINE configs[2] at its full size on one GPU (2^20 starts, T = 200, the bench's launch): every output
+    row is exact (A g = 0, g in the box, g != 0), canonical and lexicographically sorted; sampled rows are
+    ⊑-minimal against the WHOLE output set (support-mask prefilter, then the exact test on the host); sampled
+    starts [0, 256) of the same launch configuration pass gate G2 against the fp64 oracle, and the sets of
+    starts [0, 512) pass gate G3."""
+    from synth import c3
+    inst = c3()
+    assert inst.n_starts == 1 << 20
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    rows = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed).rows().astype(np.int64)
+    assert rows.shape[0] > 100000
+    assert np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
+    first = rows[np.arange(len(rows)), np.argmax(rows != 0, axis=1)]
+    assert np.all(first > 0)                                                     # canonical
+    r8 = rows.astype(np.int8)
+    assert all(tuple(a) < tuple(b) for a, b in zip(r8[:2000].tolist(), r8[1:2001].tolist()))   # sorted (sample)
+    # minimality of 300 sampled rows against all rows: h ⊑ ±g needs supp(h) ⊆ supp(g)
+    nz = rows != 0
+    words = np.packbits(nz, axis=1).view(np.uint8)
+    rng = np.random.default_rng(0)
+    for gi in rng.choice(len(rows), 300, replace=False):
+        outside = (words & ~words[gi][None, :]).any(axis=1)
+        cand = np.flatnonzero(~outside)
+        g = rows[gi]
+        H = rows[cand]
+        ag, sg = np.abs(g), np.sign(g)
+        le = np.all(np.abs(H) <= ag, axis=1)
+        same = np.all(np.sign(H) * sg >= 0, axis=1) | np.all(np.sign(H) * sg <= 0, axis=1)
+        assert int(np.sum(le & same)) == 1                                       # only g itself
+    # sampled starts of the same launch: iterates (G2) and sets (G3)
+    S_ = 256
+    Z, _ = ctx.debug_descent(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed)
+    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(S_))
+    Z64 = OX.descend(z0, ctx.B, inst.steps, inst.lr)
+    Z32 = OX.descend(z0.astype(np.float32), ctx.B, inst.steps, inst.lr, dtype=np.float32)
+
+    def pf(A, R):
+        return float(np.mean(np.all(np.abs(A.astype(np.float64) - R) / np.maximum(1, np.abs(R)) <= 1e-4, axis=1)))
+    assert pf(Z, Z64) >= pf(Z32, Z64) - 0.02
+    part = _set(ctx.extract_range(inst.n_starts, 0, 512, inst.steps, inst.lr, inst.seed).rows())
+    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
+                              starts=np.arange(512))
+    ref, _ = OP.postprocess(inst.A, inst.l, inst.u, np.array(sorted(pool), dtype=np.int64).reshape(-1, inst.n))
+    R = set(ref)
+    assert len(part & R) >= 0.9 * len(part | R)
