@@ -109,6 +109,7 @@ struct maple_ctx {
     double lam1 = 0.85, lam2 = 1.0, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
     int filter_minimal = 1;
     int descent_kernel = 0;
+    bool sb_ready = false;        // SIMT schedules built (build_sparse)
     int filter_algo = 0;          // 0 auto (indexed), 1 tiled, 2 indexed
     int optimizer = 0;            // reading #24: 0 Adam, 1 GD, 2 sign-GD
     int harvest_final = 0;        // reading #25: 1 = harvest the final iterate only
@@ -163,12 +164,27 @@ enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_N
 
 namespace {
 
+// maple_create's uploads go through this thread's pinned staging buffer as asynchronous copies (a pageable
+// cudaMemcpy blocks per call); maple_create resets it on entry and synchronises the device before returning,
+// so the buffer is free again for the thread's next create.
+thread_local HostStage t_upload_stage;
+
 template <class T>
 cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
     cudaError_t e = b.ensure(std::max<size_t>(1, v.size()) * sizeof(T));
     if (e != cudaSuccess) return e;
     if (v.empty()) return cudaSuccess;
-    return cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    const size_t nb = v.size() * sizeof(T);
+    HostStage& st = t_upload_stage;
+    size_t off = (st.used + 15) & ~size_t(15);
+    if (off + nb > st.bytes) {   // grow: the copies still reading the old buffer must finish first
+        if ((e = cudaStreamSynchronize(g_alloc_stream)) != cudaSuccess) return e;
+        if ((e = st.reserve(std::max(2 * st.bytes, nb + 4096))) != cudaSuccess) return e;
+        off = 0;
+    }
+    std::memcpy(st.p + off, v.data(), nb);
+    st.used = off + nb;
+    return cudaMemcpyAsync(b.p, st.p + off, nb, cudaMemcpyHostToDevice, g_alloc_stream);
 }
 
 unsigned long long* counters(maple_ctx* c) { return c->counters.as<unsigned long long>(); }
@@ -391,6 +407,87 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     return p;
 }
 
+// Sparse B for the SIMT descent: lane-major, bank-scheduled ELL words (sparse_ell.h), uploaded on the
+// context's allocation stream.
+int build_sparse(maple_ctx* ctx) {
+    const int n = ctx->n, d = ctx->d;
+    {
+        std::vector<std::vector<std::pair<int, int>>> rows(n), cols(d);
+        int nnz = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < d; ++j) {
+                const int v = (int)ctx->B[(size_t)i * d + j];
+                if (!v) continue;
+                rows[i].emplace_back(j, v);
+                cols[j].emplace_back(i, v);
+                ++nnz;
+            }
+        // forward lists longer than a quarter of a lane's share are split (the rows of a kernel basis are
+        // uneven: C3's longest has 91 nonzeros against 38 per lane); columns stay whole (Adam ownership)
+        if (std::max(n, d) > kEllMaxIndex) return MAPLE_ERR_RANGE;
+        const int chunk = std::max(4, ((nnz + 31) / 32 + 3) / 4);
+        // Storage in owner order: coordinate j of z (and of r = round(z)) lives at its backward place q*32 + L
+        // (lane L owns it for Adam), row i of s = sign(Bz) (and of the harvested g) at its forward place; split
+        // rows after the qf*32 places. Adam and the forward stores then touch contiguous, conflict-free words,
+        // and a gather's bank is the owner lane of what it gathers. The lane assignment depends only on the
+        // list lengths, so a first pass fixes the places and the second schedules the remapped gathers.
+        const EllSchedule F0 = build_ell(rows, d, chunk);
+        const EllSchedule B0 = build_ell(cols, n, 0);
+        const int qf0 = std::max(F0.max_pieces, 1), qd0 = std::max(B0.max_pieces, 1);
+        std::vector<int> pz(d, -1), ps(n, -1);
+        for (size_t k = 0; k < B0.owned.size(); ++k)
+            if (B0.owned[k] >= 0) pz[B0.owned[k]] = (int)k;
+        for (size_t k = 0; k < F0.owned.size(); ++k)
+            if (F0.owned[k] >= 0) ps[F0.owned[k]] = (int)k;
+        for (size_t f3 = 0; f3 < F0.fixup.size(); f3 += 3) ps[F0.fixup[f3]] = qf0 * 32 + (int)(f3 / 3);
+        auto remap = [](std::vector<std::vector<std::pair<int, int>>> L, const std::vector<int>& pos) {
+            for (auto& l : L)
+                for (auto& e : l) e.first = pos[e.first];
+            return L;
+        };
+        const EllSchedule F = build_ell(remap(rows, pz), qd0 * 32, chunk);
+        const EllSchedule Bk = build_ell(remap(cols, ps), qf0 * 32 + (int)F0.fixup.size() / 3, 0);
+        if (F.owned != F0.owned || Bk.owned != B0.owned || F.fixup != F0.fixup) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        for (int i = 0; i < n; ++i)
+            if (ps[i] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        for (int j = 0; j < d; ++j)
+            if (pz[j] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
+        CU(upload(ctx->ell_pos_s, std::vector<int32_t>(ps.begin(), ps.end())));
+        CU(upload(ctx->ell_pos_z, std::vector<int32_t>(pz.begin(), pz.end())));
+        std::vector<int32_t> fix = F.fixup, fixpos = F.fixpos;
+        if (fix.empty()) fix.push_back(0);
+        if (fixpos.empty()) fixpos.push_back(0);
+        CU(upload(ctx->ell_f, F.words));
+        CU(upload(ctx->ell_own_f, F.owned));
+        CU(upload(ctx->ell_fix, fix));
+        CU(upload(ctx->ell_fixpos, fixpos));
+        CU(upload(ctx->ell_b, Bk.words));
+        CU(upload(ctx->ell_owned, Bk.owned));
+        SparseB& sb = ctx->sb;
+        sb.nnz = nnz;
+        sb.Lf = F.slots;
+        sb.qf = F.max_pieces;
+        sb.nfix = (int)F.fixup.size() / 3;
+        sb.nfixpos = (int)F.fixpos.size();
+        sb.Lb = Bk.slots;
+        sb.qd = Bk.max_pieces;
+        sb.ell_f = ctx->ell_f.as<uint32_t>();
+        sb.own_f = ctx->ell_own_f.as<int32_t>();
+        sb.fix = ctx->ell_fix.as<int32_t>();
+        sb.fixpos = ctx->ell_fixpos.as<int32_t>();
+        sb.ell_b = ctx->ell_b.as<uint32_t>();
+        sb.own_b = ctx->ell_owned.as<int32_t>();
+        sb.pos_s = ctx->ell_pos_s.as<int32_t>();
+        sb.pos_z = ctx->ell_pos_z.as<int32_t>();
+        ctx->ell_conflicts = F.conflicts + Bk.conflicts;
+    }
+    // the staged copies must land before the staging buffer is reused (a lazy build runs inside an extraction)
+    CU(cudaStreamSynchronize(g_alloc_stream));
+    t_upload_stage.used = 0;
+    ctx->sb_ready = true;
+    return MAPLE_OK;
+}
+
 constexpr int kAutoTc = 2;   // auto choice for tensor-core shapes
 
 // the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start)
@@ -470,6 +567,10 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     if (cudaSetDevice(device) != cudaSuccess) return MAPLE_ERR_CUDA;
     ctx->device = device;
     g_alloc_stream = 0;
+    if (t_upload_stage.used) {   // a previous create of this thread that failed early may still be copying
+        cudaStreamSynchronize(0);
+        t_upload_stage.used = 0;
+    }
     {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -545,75 +646,11 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->B_dn, bdn));
     CU(upload(ctx->B8, b8));
     CU(upload(ctx->dBp, ctx->Bp));
-    {   // sparse B: lane-major, bank-scheduled ELL words for the SIMT path (sparse_ell.h)
-        std::vector<std::vector<std::pair<int, int>>> rows(n), cols(d);
-        int nnz = 0;
-        for (int i = 0; i < n; ++i)
-            for (int j = 0; j < d; ++j) {
-                const int v = (int)ctx->B[(size_t)i * d + j];
-                if (!v) continue;
-                rows[i].emplace_back(j, v);
-                cols[j].emplace_back(i, v);
-                ++nnz;
-            }
-        // forward lists longer than a quarter of a lane's share are split (the rows of a kernel basis are
-        // uneven: C3's longest has 91 nonzeros against 38 per lane); columns stay whole (Adam ownership)
-        if (std::max(n, d) > kEllMaxIndex) return MAPLE_ERR_RANGE;
-        const int chunk = std::max(4, ((nnz + 31) / 32 + 3) / 4);
-        // Storage in owner order: coordinate j of z (and of r = round(z)) lives at its backward place q*32 + L
-        // (lane L owns it for Adam), row i of s = sign(Bz) (and of the harvested g) at its forward place; split
-        // rows after the qf*32 places. Adam and the forward stores then touch contiguous, conflict-free words,
-        // and a gather's bank is the owner lane of what it gathers. The lane assignment depends only on the
-        // list lengths, so a first pass fixes the places and the second schedules the remapped gathers.
-        const EllSchedule F0 = build_ell(rows, d, chunk);
-        const EllSchedule B0 = build_ell(cols, n, 0);
-        const int qf0 = std::max(F0.max_pieces, 1), qd0 = std::max(B0.max_pieces, 1);
-        std::vector<int> pz(d, -1), ps(n, -1);
-        for (size_t k = 0; k < B0.owned.size(); ++k)
-            if (B0.owned[k] >= 0) pz[B0.owned[k]] = (int)k;
-        for (size_t k = 0; k < F0.owned.size(); ++k)
-            if (F0.owned[k] >= 0) ps[F0.owned[k]] = (int)k;
-        for (size_t f3 = 0; f3 < F0.fixup.size(); f3 += 3) ps[F0.fixup[f3]] = qf0 * 32 + (int)(f3 / 3);
-        auto remap = [](std::vector<std::vector<std::pair<int, int>>> L, const std::vector<int>& pos) {
-            for (auto& l : L)
-                for (auto& e : l) e.first = pos[e.first];
-            return L;
-        };
-        const EllSchedule F = build_ell(remap(rows, pz), qd0 * 32, chunk);
-        const EllSchedule Bk = build_ell(remap(cols, ps), qf0 * 32 + (int)F0.fixup.size() / 3, 0);
-        if (F.owned != F0.owned || Bk.owned != B0.owned || F.fixup != F0.fixup) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
-        for (int i = 0; i < n; ++i)
-            if (ps[i] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
-        for (int j = 0; j < d; ++j)
-            if (pz[j] < 0) return MAPLE_ERR_RANGE;   // (cannot happen: the lane assignment depends on list lengths only)
-        CU(upload(ctx->ell_pos_s, std::vector<int32_t>(ps.begin(), ps.end())));
-        CU(upload(ctx->ell_pos_z, std::vector<int32_t>(pz.begin(), pz.end())));
-        std::vector<int32_t> fix = F.fixup, fixpos = F.fixpos;
-        if (fix.empty()) fix.push_back(0);
-        if (fixpos.empty()) fixpos.push_back(0);
-        CU(upload(ctx->ell_f, F.words));
-        CU(upload(ctx->ell_own_f, F.owned));
-        CU(upload(ctx->ell_fix, fix));
-        CU(upload(ctx->ell_fixpos, fixpos));
-        CU(upload(ctx->ell_b, Bk.words));
-        CU(upload(ctx->ell_owned, Bk.owned));
-        SparseB& sb = ctx->sb;
-        sb.nnz = nnz;
-        sb.Lf = F.slots;
-        sb.qf = F.max_pieces;
-        sb.nfix = (int)F.fixup.size() / 3;
-        sb.nfixpos = (int)F.fixpos.size();
-        sb.Lb = Bk.slots;
-        sb.qd = Bk.max_pieces;
-        sb.ell_f = ctx->ell_f.as<uint32_t>();
-        sb.own_f = ctx->ell_own_f.as<int32_t>();
-        sb.fix = ctx->ell_fix.as<int32_t>();
-        sb.fixpos = ctx->ell_fixpos.as<int32_t>();
-        sb.ell_b = ctx->ell_b.as<uint32_t>();
-        sb.own_b = ctx->ell_owned.as<int32_t>();
-        sb.pos_s = ctx->ell_pos_s.as<int32_t>();
-        sb.pos_z = ctx->ell_pos_z.as<int32_t>();
-        ctx->ell_conflicts = F.conflicts + Bk.conflicts;
+    // the SIMT schedules are built now only when the SIMT kernel is the automatic choice; a tcgen05-shaped
+    // context builds them on its first SIMT launch (maple_set_descent_kernel(1))
+    if (!(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0)) {
+        const int rc = build_sparse(ctx);
+        if (rc) return rc;
     }
     CU(upload(ctx->th_off, toff));
     CU(upload(ctx->th_c0, wc0));
@@ -807,6 +844,10 @@ int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
         for (int64_t c0 = begin; c0 < end; c0 += chunk_max) {
             const int64_t cnt = std::min(chunk_max, end - c0);
             CU(cudaMemsetAsync(counters(ctx) + C_CAND, 0, 8, s));
+            if (which_descent(ctx) == 1 && !ctx->sb_ready) {
+                rc = build_sparse(ctx);
+                if (rc) return rc;
+            }
             DescentParams p = descent_params(ctx, steps, seed, n_starts, c0, cnt);
             p.harvest = 1;
             p.cand = ctx->cand.as<int8_t>();
@@ -945,6 +986,10 @@ int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
     if (cnt == 0) return MAPLE_OK;
     CU(ctx->zout.ensure((size_t)cnt * ctx->d * sizeof(float)));
     CU(ctx->z0out.ensure((size_t)cnt * ctx->d * sizeof(double)));
+    if (which_descent(ctx) == 1 && !ctx->sb_ready) {
+        rc = build_sparse(ctx);
+        if (rc) return rc;
+    }
     DescentParams p = descent_params(ctx, steps, seed, n_starts, begin, cnt);
     p.harvest = 0;
     p.Z_out = ctx->zout.as<float>();
