@@ -159,7 +159,18 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     for (int t = 0; t < p.T; ++t) {
         // forward: s_i = sign((B z)_i)
         ell_run(wf, Lf, zsh, res + lane);
-        ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int pl, int, float y) { ssh[pl] = fsign(y); });
+        // s = sign(Bz): whole rows sit at their queue place (owner order), so every place is converted without
+        // looking up its row (places of split pieces get a value no gather reads); split rows via the fixups
+        for (int q = 0; q < sb.qf; ++q) ssh[q * 32 + lane] = fsign(res[q * 32 + lane]);
+        if (sb.nfix) {
+            __syncwarp();
+            for (int f = lane; f < sb.nfix; f += 32) {
+                const int b = fix[3 * f + 1], c = fix[3 * f + 2];
+                float acc = 0.f;
+                for (int k = 0; k < c; ++k) acc += res[fixpos[b + k]];
+                ssh[sb.qf * 32 + f] = fsign(acc);
+            }
+        }
         // lowest-index argmax of |z| (λ2 term, Eq. 3), over this lane's coordinates then the warp
         float best = -1.f;
         int bestj = 0x7fffffff, bestp = 0;
