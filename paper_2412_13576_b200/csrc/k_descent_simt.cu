@@ -217,7 +217,12 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             const int pl = q * 32 + lane;
             const float zz = zsh[pl];
             // (the queue slot of an unused place may hold a forward piece sum: read 0 there)
-            float gr = (j >= 0 ? res[q * 32 + lane] : 0.f) + lam1 * (ceilf(zz) + floorf(zz) - 2.f * zz);
+            // λ1 d/dz (z - floor z)(ceil z - z) = ceil z + floor z - 2z = sign(z - r) - 2 (z - r), r = round(z)
+            // (z - r is exact; both forms round the same real value once), r also serves the change test
+            const float ro = round_half_away_f(zz);
+            const float dd = zz - ro;
+            const float sd = dd != 0.f ? copysignf(1.f, dd) : 0.f;
+            float gr = fmaf(lam1, fmaf(-2.f, dd, sd), j >= 0 ? res[q * 32 + lane] : 0.f);
             gr += (j == bestj) ? extra : 0.f;
             float zn;
             if (opt == 0) {   // Adam (reading #9)
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             }
             zsh[pl] = zn;
             const float rn = round_half_away_f(zn);
-            changed |= rn != round_half_away_f(zz);
+            changed |= rn != ro;
             grsh[pl] = rn;
         }
         __syncwarp();
