@@ -1,6 +1,7 @@
 """Graver-best augmentation (Alg. 2) and MAPLE's multi-start best (§4.3) — oracle.
 
-Objective convention f(x) = 1/2 x^T Q x + c^T x + c0 (reading #20). When Q, c and c0 are
+Objective convention f(x) = 1/2 x^T Q x + c^T x + c0 (reading #20), or a separable
+f(x) = c0 + sum_j f_j(x_j) given by value tables over the box (Prop. 3; reading #27). When Q, c and c0 are
 integer-valued the comparison uses 2 f(x) in exact Python integers (no rounding at all); otherwise fp64.
 
 Readings: #17 steps (g, lambda) with g in D = S ∪ -S (both signs), lambda in Z_+ = {1, 2, ...},
@@ -10,6 +11,8 @@ over f(x + lambda g) breaks ties by lexicographically smallest g (in D's sorted 
 guards wide boxes). #19 the multi-start best breaks ties by lexicographically smallest x.
 """
 from __future__ import annotations
+
+import math
 
 import numpy as np
 
@@ -54,6 +57,30 @@ class Objective:
     def value(self, x) -> float:
         k = self.key(x)
         return k / 2.0 if self.exact else k
+
+
+class SeparableTable:
+    """f(x) = c0 + sum_j f_j(x_j) (the separable form of Prop. 3), each f_j given by its values on the
+    integer box: tables[j][k] = f_j(l_j + k). Evaluated by its definition: an exact integer sum when every
+    value is integral, else the correctly rounded fp64 sum (math.fsum)."""
+
+    def __init__(self, tables, l, c0=0.0):
+        self.tables = [np.asarray(t, dtype=np.float64) for t in tables]
+        self.l = [int(v) for v in l]
+        self.c0 = float(c0)
+        self.exact = all(_integral(t) for t in self.tables) and _integral([self.c0])
+        if self.exact:
+            self.ti = [[int(round(v)) for v in t] for t in self.tables]
+            self.c0i = int(round(self.c0))
+
+    def key(self, x):
+        idx = [int(v) - lj for v, lj in zip(x, self.l)]
+        if self.exact:
+            return self.c0i + sum(t[k] for t, k in zip(self.ti, idx))
+        return math.fsum([self.c0] + [float(t[k]) for t, k in zip(self.tables, idx)])
+
+    def value(self, x) -> float:
+        return float(self.key(x))
 
 
 def max_step_length(x, g, l, u) -> int:

@@ -117,3 +117,62 @@ def test_exact_integer_objective():
     assert f.key(x) == int(x @ np.array([[2, 1], [1, 2]]) @ x + 2 * (3 * 4 + 7) + 10)
     g = AU.Objective(np.eye(2) * 0.5, [0.1, 0.2])
     assert not g.exact and g.value([1, 1]) == pytest.approx(0.5 + 0.3)
+
+
+# ---- separable value tables (reading #27; Prop. 3: f(x) = sum_j f_j(x^j)) ----
+
+def _tables(fns, l, u):
+    return [[fj(t) for t in range(int(a), int(c) + 1)] for fj, a, c in zip(fns, l, u)]
+
+
+def test_table_worked_value():
+    """SeparableConvex f_j(t) = (t - 2)^2, x = (3, 1) -> 1 + 1 = 2."""
+    f = AU.SeparableTable(_tables([lambda t: (t - 2) ** 2] * 2, [0, 0], [3, 3]), [0, 0])
+    assert f.exact and f.value((3, 1)) == 2.0
+    assert AU.SeparableTable(_tables([lambda t: (t - 2) ** 2] * 2, [-1, 1], [3, 3]), [-1, 1]).value((3, 1)) == 2.0
+
+
+def test_table_matches_diagonal_quadratic():
+    """The table of 1/2 q_j t^2 + c_j t is the SEPARABLE quadratic (Objective with diag Q): same ordering on
+    every point of a box with a nonzero lower bound (catches an offset / index slip in the table lookup)."""
+    rng = np.random.default_rng(4)
+    n = 4
+    l, u = rng.integers(-3, 1, size=n), rng.integers(1, 4, size=n)
+    q, c = rng.integers(1, 5, size=n), rng.integers(-6, 7, size=n)
+    fq = AU.Objective(np.diag(q).astype(float), c.astype(float), 3.0)
+    ft = AU.SeparableTable(_tables([lambda t, a=a, b=b: 0.5 * a * t * t + b * t for a, b in zip(q, c)], l, u), l, 3.0)
+    for p in itertools.product(*[range(int(a), int(b) + 1) for a, b in zip(l, u)]):
+        assert ft.value(p) == fq.value(p)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_prop3_table_convex_nonquadratic_reaches_optimum(seed):
+    """Prop. 3 beyond quadratics: with the true Graver basis, augmentation on separable convex
+    non-quadratic f_j (|t - a|^3, piecewise-linear max(w1 (a - t), w2 (t - a)), and 2^|t - a|) reaches the
+    brute-force optimum from every feasible start."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.integers(3, 6))
+    m = int(rng.integers(1, 3))
+    A = rng.integers(-2, 3, size=(m, n))
+    if np.linalg.matrix_rank(A.astype(float)) < m:
+        A[0, 0] = 7
+    l, u = np.zeros(n, np.int64), np.full(n, 3)
+    b = A @ rng.integers(0, 4, size=n)
+    fns = []
+    for j in range(n):
+        a = float(rng.integers(0, 4)) + 0.5 * float(rng.integers(0, 2))
+        kind = int(rng.integers(0, 3))
+        if kind == 0:
+            fns.append(lambda t, a=a: abs(t - a) ** 3)
+        elif kind == 1:
+            w1, w2 = int(rng.integers(1, 6)), int(rng.integers(1, 6))
+            fns.append(lambda t, a=a, w1=w1, w2=w2: max(w1 * (a - t), w2 * (t - a)))
+        else:
+            fns.append(lambda t, a=a: 2.0 ** abs(t - a))
+    f = AU.SeparableTable(_tables(fns, l, u), l, c0=1.25)
+    S = {Gv.canonical(g) for g in Gv.graver_in_box(A, -(u - l), u - l)}
+    feas, opt = _brute_optimum(f, A, b, l, u)
+    for x0 in feas[:: max(1, len(feas) // 6)]:
+        x, _ = AU.graver_best_augment(f, A, b, l, u, x0, S)
+        assert AU.feasible(A, b, l, u, x)
+        assert f.key(x) == opt
