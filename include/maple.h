@@ -49,6 +49,13 @@ extern "C" {
 /* objective kinds for maple_objective.kind */
 #define MAPLE_OBJ_QUADRATIC        0   /* f(x) = 1/2 x^T Q x + c^T x + c0, Q dense n x n */
 #define MAPLE_OBJ_SEPARABLE        1   /* same with Q diagonal: Q points to the n diagonal entries */
+/* Separable f(x) = c0 + sum_j f_j(x_j) with ANY real f_j (Prop. 3: G(A) is a test set when every
+ * f_j is convex), given by its values on the integer box: Q points to sum_j (u_j - l_j + 1) doubles, the
+ * table of coordinate j starting at offset sum_{i<j} (u_i - l_i + 1), entry k = f_j(l_j + k); c is ignored
+ * (may be NULL). Scores are f(x + lambda g) - f(x) = sum over the support of g, ascending j, of
+ * f_j(x_j + lambda g_j) - f_j(x_j) in fp64 (exact for integer tables below 2^53). The box must hold at most
+ * 2^27 table entries. Cannot be mixed with the quadratic kinds in one maple_augment_many batch (BAD_ARG). */
+#define MAPLE_OBJ_TABLE            2
 
 #define MAPLE_MAX_N             1024   /* device row encoding limit on n */
 
@@ -56,9 +63,10 @@ typedef struct maple_ctx maple_ctx;
 typedef struct maple_dirset maple_dirset;
 
 typedef struct maple_objective {
-    int32_t kind;          /* MAPLE_OBJ_QUADRATIC or MAPLE_OBJ_SEPARABLE */
-    const double* Q;       /* host; n*n row-major (QUADRATIC) or n (SEPARABLE); must be symmetric */
-    const double* c;       /* host; n */
+    int32_t kind;          /* MAPLE_OBJ_QUADRATIC, MAPLE_OBJ_SEPARABLE or MAPLE_OBJ_TABLE */
+    const double* Q;       /* host; n*n row-major (QUADRATIC, symmetrised), n (SEPARABLE) or the value table
+                              (TABLE, sum_j (u_j - l_j + 1) entries) */
+    const double* c;       /* host; n (ignored for TABLE) */
     double c0;
 } maple_objective;
 

@@ -117,7 +117,7 @@ struct maple_ctx {
     DevBuf ffreq, fkey, fbh, fbs, fbc, flrow, flsig;   // indexed filter (k_post.cu)
     DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, sig, l1, hist, level_start, cursor, order, keep,
         witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
-    DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b;
+    DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b, atab, atoff;
     int64_t cand_cap = 0, pool_cap = 0, want_cand = 0, want_pool = 0;
     bool timings_pending = false;
     uint64_t table_slots = 0;
@@ -694,7 +694,7 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
                       &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,
-                      &ctx->af2b};
+                      &ctx->af2b, &ctx->atab, &ctx->atoff};
     for (DevBuf* b : bufs) b->release();
     cudaStreamSynchronize(ctx->stream);
     ctx->stage_aug.release();
@@ -1021,9 +1021,22 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
                 if (acc != b[(size_t)t * m + r]) FAIL(MAPLE_ERR_INFEASIBLE, "x0 violates A x = b");
             }
         }
-    for (int t = 0; t < n_inst; ++t)
-        if (!f[t].c || !f[t].Q || (f[t].kind != MAPLE_OBJ_QUADRATIC && f[t].kind != MAPLE_OBJ_SEPARABLE))
+    const bool table = n_inst > 0 && f[0].kind == MAPLE_OBJ_TABLE;
+    for (int t = 0; t < n_inst; ++t) {
+        if (!f[t].Q || (f[t].kind != MAPLE_OBJ_QUADRATIC && f[t].kind != MAPLE_OBJ_SEPARABLE &&
+                        f[t].kind != MAPLE_OBJ_TABLE))
             FAIL(MAPLE_ERR_BAD_ARG, "bad objective");
+        if ((f[t].kind == MAPLE_OBJ_TABLE) != table) FAIL(MAPLE_ERR_BAD_ARG, "mixed objective kinds in one batch");
+        if (!table && !f[t].c) FAIL(MAPLE_ERR_BAD_ARG, "bad objective");
+    }
+    // separable value tables (MAPLE_OBJ_TABLE): coordinate j's table starts at sum_{i<j} (u_i - l_i + 1)
+    std::vector<int32_t> toff(n);
+    int64_t tab_len = 0;
+    for (int i = 0; i < n && table; ++i) {
+        toff[i] = (int32_t)tab_len;
+        tab_len += (int64_t)ctx->u[i] - ctx->l[i] + 1;
+        if (tab_len > (int64_t(1) << 27)) FAIL(MAPLE_ERR_BAD_ARG, "value table longer than 2^27 entries");
+    }
     CU(cudaEventRecord(ctx->ev[8], s));
     maple_dirset* dsm = const_cast<maple_dirset*>(ds);
     const int64_t K = ds->size;
@@ -1041,15 +1054,20 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     }
     // objective data (dense Q per instance), staged in pinned memory
     const int64_t ninc = (int64_t)n_inst * k0;
-    const size_t nQ = (size_t)n_inst * n * n, nc = (size_t)n_inst * n;
-    CU(ctx->stage_aug.reserve(nQ * 8 + nc * 8 + (size_t)n_inst * 8 + (size_t)ninc * n * 4 + 64));
+    const size_t nQ = table ? (size_t)n_inst * tab_len : (size_t)n_inst * n * n, nc = (size_t)n_inst * n;
+    CU(ctx->stage_aug.reserve(nQ * 8 + nc * 8 + (size_t)n_inst * 8 + (size_t)ninc * n * 4 + (size_t)n * 4 + 128));
     double* Q = ctx->stage_aug.take<double>(nQ);
     double* c = ctx->stage_aug.take<double>(nc);
     double* c0 = ctx->stage_aug.take<double>(n_inst);
     int32_t* X0 = ctx->stage_aug.take<int32_t>((size_t)ninc * n);
-    std::memset(Q, 0, nQ * 8);
+    if (!table) std::memset(Q, 0, nQ * 8);
     std::memcpy(X0, x0, (size_t)ninc * n * 4);
     for (int t = 0; t < n_inst; ++t) {
+        if (table) {   // the tables as given; c unused
+            std::memcpy(Q + (size_t)t * tab_len, f[t].Q, sizeof(double) * tab_len);
+            c0[t] = f[t].c0;
+            continue;
+        }
         double* Qt = Q + (size_t)t * n * n;
         if (f[t].kind == MAPLE_OBJ_QUADRATIC) {
             // the kernels use grad = Q x + c, which is the gradient of 1/2 x^T Q x only for symmetric Q:
@@ -1075,6 +1093,12 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     CU(cudaMemcpyAsync(ctx->ac.p, c, nc * 8, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(ctx->ac0.p, c0, (size_t)n_inst * 8, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync(ctx->aX.p, X0, (size_t)ninc * n * 4, cudaMemcpyHostToDevice, s));
+    if (table) {
+        int32_t* toff_h = ctx->stage_aug.take<int32_t>(n);
+        std::memcpy(toff_h, toff.data(), (size_t)n * 4);
+        CU(ctx->atoff.ensure((size_t)n * 4));
+        CU(cudaMemcpyAsync(ctx->atoff.p, toff_h, (size_t)n * 4, cudaMemcpyHostToDevice, s));
+    }
     AugmentParams p{};
     p.n = n;
     p.m = m;
@@ -1096,8 +1120,12 @@ static int augment_impl(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, 
     p.F2 = ctx->aF2.as<double>();
     p.iters = ctx->aIt.as<int32_t>();
     p.max_iter = 1 << 20;
+    p.table = table ? 1 : 0;
+    p.tab = ctx->aQ.as<double>();   // TABLE: the staged value tables
+    p.tab_off = ctx->atoff.as<int32_t>();
+    p.tab_len = tab_len;
     CU(launch_augment_qg(p, s));
-    ctx->launches++;
+    if (!table) ctx->launches++;
     CU(cudaEventRecord(ctx->ev[9], s));
     CU(launch_augment(p, s));
     CU(launch_augment_best(p, ctx->axb.as<int32_t>(), ctx->af2b.as<double>(), s));

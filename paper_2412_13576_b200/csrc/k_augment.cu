@@ -7,6 +7,9 @@
 // 1..λmax(x, g) that keep l <= x + λg <= u (A g = 0 keeps A x = b). The CTA takes the argmin over
 // (2Δ, index of g in D, λ) among strict improvements 2Δ < 0 — the paper's argmin with the tie-break of
 // reading #17 — applies x += λg and ∇ += λ Q g, and stops when no improving step exists.
+// Separable value tables (MAPLE_OBJ_TABLE; Prop. 3): f(x) = c0 + sum_j f_j(x_j) with f_j read from a
+// table over [l_j, u_j], so f(x + λg) - f(x) = sum over the support of g (ascending j) of
+// f_j(x_j + λ g_j) - f_j(x_j), and 2Δ of that sum is the key (no gradient state).
 // Directions are kept in ELL form (nonzero columns + values, Graver elements are sparse), so the score,
 // the step bound and the gradient update all cost O(nnz(g)) instead of O(n).
 #include <algorithm>
@@ -96,6 +99,7 @@ augment_kernel(AugmentParams p, int staged) {
     const double* Q = p.Q + (size_t)inst * n * n;
     const double* c = p.c + (size_t)inst * n;
     const double* qg = p.qg + (size_t)inst * 2 * p.n_dir;
+    const double* tab = p.tab + (size_t)inst * p.tab_len;
     int32_t* xg = p.X + (size_t)inc * n;
     if (staged) {
         const int nD2 = 2 * p.n_dir, nz = p.nzmax;
@@ -117,14 +121,18 @@ augment_kernel(AugmentParams p, int staged) {
         dn[i] = x[i] - p.lo[i];
     }
     __syncthreads();
-    // ∇ = Q x + c ; 2 f(x) = x^T Q x + 2 c^T x + 2 c0
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    // ∇ = Q x + c ; 2 f(x) = x^T Q x + 2 c^T x + 2 c0   (tables: 2 f(x) = 2 (c0 + sum_j f_j(x_j)))
+    for (int i = threadIdx.x; i < n && !p.table; i += blockDim.x) {
         double acc = c[i];
         for (int j = 0; j < n; ++j) acc += Q[(size_t)i * n + j] * (double)x[j];
         grad[i] = acc;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && p.table) {
+        double f = p.c0[inst];
+        for (int i = 0; i < n; ++i) f += tab[p.tab_off[i] + dn[i]];
+        f2_sh = 2.0 * f;
+    } else if (threadIdx.x == 0) {
         double f2 = 2.0 * p.c0[inst];
         for (int i = 0; i < n; ++i) f2 += (double)x[i] * (grad[i] + c[i]);  // x^T(Qx + c) + c^T x
         f2_sh = f2;
@@ -148,6 +156,24 @@ augment_kernel(AugmentParams p, int staged) {
                 if (lmax < 1 || (w & kEnd)) break;
             }
             if (lmax < 1) continue;
+            if (p.table) {
+                for (int lam = 1; lam <= lmax; ++lam) {
+                    double dlt = 0.0;
+                    for (int a = 0;; ++a) {
+                        const uint32_t w = we[(size_t)a * nD];
+                        const int i = wcol(w);
+                        const double* ti = tab + p.tab_off[i] + dn[i];
+                        dlt += ti[lam * wval(w)] - ti[0];
+                        if (w & kEnd) break;
+                    }
+                    const double key = 2.0 * dlt;
+                    if (key < 0.0) {
+                        Cand cnd{key, e, lam};
+                        if (better(cnd, mine)) mine = cnd;
+                    }
+                }
+                continue;
+            }
             double s = 0.0;
             for (int a = 0;; ++a) {
                 const uint32_t w = we[(size_t)a * nD];
@@ -186,7 +212,7 @@ augment_kernel(AugmentParams p, int staged) {
         const int k = p.nnz[b.e];
         const uint32_t* wb = p.words + b.e;
         // ∇ += λ Q g (Q symmetric: column i of Q = row i, read coalesced)
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int i = threadIdx.x; i < n && !p.table; i += blockDim.x) {
             double acc = 0.0;
             for (int a = 0; a < k; ++a) {
                 const uint32_t w = wb[(size_t)a * nD];
@@ -280,6 +306,7 @@ cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* 
 }
 
 cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s) {
+    if (p.table) return cudaSuccess;   // tables: no quadratic form
     const int64_t total = (int64_t)2 * p.n_dir * p.n_inst;
     if (total <= 0) return cudaSuccess;
     int64_t blocks = (total + 255) / 256;

@@ -165,6 +165,10 @@ struct AugmentParams {
     const double* c;              // n (per instance)
     const double* c0;             // per instance
     const double* qg;             // per instance: g^T Q g for every D entry (2K)
+    int table;                    // 1: separable value tables (MAPLE_OBJ_TABLE) instead of Q, c
+    const double* tab;            // per instance: tab + inst * tab_len; entry tab_off[j] + (x_j - l_j) = f_j(x_j)
+    const int32_t* tab_off;       // n offsets (shared: l, u are the context's)
+    int64_t tab_len;
     const int32_t* lo;
     const int32_t* hi;
     int32_t* X;                   // incumbents, (n_inst * k0) x n, updated in place

@@ -21,7 +21,7 @@ ERRORS = {
     -1: "BAD_ARG", -2: "BAD_BOUNDS", -3: "RANK_DEFICIENT", -4: "FULL_RANK", -5: "OVERFLOW", -6: "RANGE",
     -7: "CUDA", -8: "OOM", -9: "CAPACITY", -10: "INFEASIBLE", -11: "COMM",
 }
-OBJ_QUADRATIC, OBJ_SEPARABLE = 0, 1
+OBJ_QUADRATIC, OBJ_SEPARABLE, OBJ_TABLE = 0, 1, 2
 STATUS_OK, STATUS_NO_FEASIBLE = 0, 1
 
 class maple_objective(C.Structure):
@@ -315,7 +315,7 @@ class Context:
     @staticmethod
     def _objective(Q, c, c0, kind):
         Q = np.ascontiguousarray(Q, dtype=np.float64)
-        c = np.ascontiguousarray(c, dtype=np.float64)
+        c = np.ascontiguousarray(np.zeros(1) if c is None else c, dtype=np.float64)   # OBJ_TABLE: c unused
         ob = maple_objective(kind, Q.ctypes.data_as(C.POINTER(C.c_double)), c.ctypes.data_as(C.POINTER(C.c_double)),
                              float(c0))
         return ob, (Q, c)
@@ -336,12 +336,14 @@ class Context:
         return xb, float(fb[0]), int(st[0]), it[:k0]
 
     def augment_many(self, ds: DirSet, Qs, cs, c0s, bs, X0s, kind=OBJ_QUADRATIC):
-        """maple_augment_many over n_inst instances sharing A and the direction set (configs[3])."""
+        """maple_augment_many over n_inst instances sharing A and the direction set (configs[3]). kind: one
+        objective kind for all instances, or one per instance (TABLE cannot be mixed with the quadratic kinds)."""
         n_inst = len(Qs)
         obs = (maple_objective * n_inst)()
         keep = []
         for t in range(n_inst):
-            ob, k = self._objective(Qs[t], cs[t], c0s[t], kind)
+            ob, k = self._objective(Qs[t], None if cs is None else cs[t], c0s[t],
+                                   kind[t] if isinstance(kind, (list, tuple)) else kind)
             obs[t] = ob
             keep.append(k)
         b = np.ascontiguousarray(np.asarray(bs, dtype=np.int32).reshape(n_inst, self.m))
