@@ -10,7 +10,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def child(lib, workload, iters):
+def child(lib, workload, iters, n_starts=0):
     sys.path.insert(0, ROOT)
     import numpy as np
     from paper_2412_13576_b200 import maple
@@ -18,11 +18,12 @@ def child(lib, workload, iters):
     maple.load(lib)
     inst = config(workload)
     ctx = maple.Context(inst.A, inst.l, inst.u, device=0)
+    N = n_starts or inst.n_starts
     for _ in range(3):
-        ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
+        ctx.extract(N, inst.steps, inst.lr, inst.seed)
     acc = {}
     for _ in range(iters):
-        ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
+        ctx.extract(N, inst.steps, inst.lr, inst.seed)
         for k, v in ctx.timings().items():
             acc.setdefault(k, []).append(v)
     print(json.dumps({k: float(np.mean(v)) for k, v in acc.items()}))
@@ -35,14 +36,15 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--n-starts", type=int, default=0)
     a = ap.parse_args()
     if a.child:
-        child(a.libs[0], a.workload, a.iters)
+        child(a.libs[0], a.workload, a.iters, a.n_starts)
         return
     for r in range(a.reps):
         for lib in a.libs:
             out = subprocess.run([sys.executable, __file__, "--child", "--workload", a.workload, "--iters",
-                                  str(a.iters), lib], capture_output=True, text=True)
+                                  str(a.iters), "--n-starts", str(a.n_starts), lib], capture_output=True, text=True)
             line = out.stdout.strip().splitlines()[-1] if out.stdout.strip() else out.stderr[-300:]
             print(f"rep {r} {os.path.basename(lib)}: {line}", flush=True)
 
