@@ -30,12 +30,38 @@ namespace {
 
 // One ELL schedule (sparse_ell.h) for this lane: wl = ell + lane, resq = res + lane; the lane's k-th completed
 // piece sum goes to resq[k * 32]. Per slot: one 128-byte line of words, one conflict-free gather, one FFMA.
+#ifndef MAPLE_ELL_BATCH
+#define MAPLE_ELL_BATCH 1
+#endif
 __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slots, const float* __restrict__ x,
                                         float* __restrict__ resq) {
     const char* xb = reinterpret_cast<const char*>(x);
     float acc = 0.f;
+    int e = 0;
+#if MAPLE_ELL_BATCH > 1
+    // words and gathers of MAPLE_ELL_BATCH slots are issued before the batch's queue stores (x and the queue are
+    // disjoint, which the compiler cannot prove: without this every gather waits for the previous slot's store)
+    constexpr int NB = MAPLE_ELL_BATCH;
+    for (; e + NB <= slots; e += NB) {
+        uint32_t w[NB];
+        float xv[NB];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) w[k] = wl[(e + k) * 32];
+#pragma unroll
+        for (int k = 0; k < NB; ++k) xv[k] = *reinterpret_cast<const float*>(xb + (w[k] & 0xFFFCu));
+#pragma unroll
+        for (int k = 0; k < NB; ++k) {
+            acc = fmaf(__uint_as_float(w[k] & 0xFFFF0000u), xv[k], acc);
+            if (w[k] & 1u) {
+                *resq = acc;
+                resq += 32;
+                acc = 0.f;
+            }
+        }
+    }
+#endif
 #pragma unroll 4
-    for (int e = 0; e < slots; ++e) {
+    for (; e < slots; ++e) {
         const uint32_t w = wl[e * 32];
         const float xv = *reinterpret_cast<const float*>(xb + (w & 0xFFFCu));
         acc = fmaf(__uint_as_float(w & 0xFFFF0000u), xv, acc);   // bf16 B entry; PAD words carry 0
