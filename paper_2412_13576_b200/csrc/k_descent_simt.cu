@@ -31,7 +31,7 @@ namespace {
 // One ELL schedule (sparse_ell.h) for this lane: wl = ell + lane, resq = res + lane; the lane's k-th completed
 // piece sum goes to resq[k * 32]. Per slot: one 128-byte line of words, one conflict-free gather, one FFMA.
 #ifndef MAPLE_ELL_BATCH
-#define MAPLE_ELL_BATCH 1
+#define MAPLE_ELL_BATCH 8
 #endif
 __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slots, const float* __restrict__ x,
                                         float* __restrict__ resq) {
