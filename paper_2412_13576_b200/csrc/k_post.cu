@@ -500,6 +500,9 @@ __global__ void bin_scatter_kernel(FilterWork fw, const unsigned long long* dcou
     }
 }
 
+#ifndef MAPLE_IDX_UNROLL
+#define MAPLE_IDX_UNROLL 1
+#endif
 // warp per row g: scan the lists of g's support coordinates (lanes stride each range), stop at the first
 // dominator found by any lane
 constexpr int kIdxThreads = 256;
@@ -535,14 +538,25 @@ __global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork f
                 nzm &= nzm - 1;
                 const int bin0 = c * (fw.Lmax + 1);
                 const int32_t lo = fw.bin_start[bin0], hi = fw.bin_start[bin0 + l1];
-                for (int32_t p0 = lo; p0 < hi; p0 += 32) {
-                    const int32_t p = p0 + lane;
-                    bool found = false;
-                    if (p < hi) {
-                        const uint4 hs = fw.list_sig[p];
-                        const uint32_t pv = (hs.x & ~gs.x) | (hs.y & ~gs.y) | (hs.z & ~gs.z) | (hs.w & ~gs.w);
-                        const uint32_t nv = (hs.x & ~gs.z) | (hs.y & ~gs.w) | (hs.z & ~gs.x) | (hs.w & ~gs.y);
-                        if (pv == 0u || nv == 0u) {
+                // MAPLE_IDX_UNROLL chunks of 32 list entries per pass: their signature loads are issued together
+                // (the loop is L2-latency bound), then the chunks are tested in order, so the witness is the
+                // first dominator in list order exactly as with one chunk per pass
+                constexpr int U = MAPLE_IDX_UNROLL;
+                bool done = false;
+                for (int32_t p0 = lo; p0 < hi && !done; p0 += 32 * U) {
+                    uint4 hs[U];
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int32_t p = p0 + 32 * k + lane;
+                        hs[k] = p < hi ? fw.list_sig[p] : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+                    }
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int32_t p = p0 + 32 * k + lane;
+                        bool found = false;
+                        const uint32_t pv = (hs[k].x & ~gs.x) | (hs[k].y & ~gs.y) | (hs[k].z & ~gs.z) | (hs[k].w & ~gs.w);
+                        const uint32_t nv = (hs[k].x & ~gs.z) | (hs[k].y & ~gs.w) | (hs[k].z & ~gs.x) | (hs[k].w & ~gs.y);
+                        if (p < hi && (pv == 0u || nv == 0u)) {
                             const uint32_t* hc = fw.codes + (size_t)fw.list_row[p] * W2;
                             uint32_t pos_v = 0, neg_v = 0;
                             for (int w = 0; w < Wh; ++w) {
@@ -552,11 +566,12 @@ __global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork f
                             }
                             found = pos_v == 0u || neg_v == 0u;
                         }
-                    }
-                    const unsigned fm = __ballot_sync(0xffffffffu, found);
-                    if (fm) {
-                        wit = fw.list_row[p0 + __ffs(fm) - 1];
-                        break;
+                        const unsigned fm = __ballot_sync(0xffffffffu, found);
+                        if (fm) {
+                            wit = fw.list_row[p0 + 32 * k + __ffs(fm) - 1];
+                            done = true;
+                            break;
+                        }
                     }
                 }
             }
