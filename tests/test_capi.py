@@ -37,6 +37,16 @@ def test_header_symbols_all_exported(maple):
     assert sorted(maple.exported_symbols()) == syms
 
 
+def test_header_constants_match_binding(maple):
+    """The binding's objective kinds and statuses are the header's #defines (include/maple.h)."""
+    src = open(os.path.join(ROOT, "include", "maple.h")).read()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+(MAPLE_[A-Z_]+)\s+(-?\d+)", src)}
+    assert defs["MAPLE_OBJ_QUADRATIC"] == maple.OBJ_QUADRATIC
+    assert defs["MAPLE_OBJ_SEPARABLE"] == maple.OBJ_SEPARABLE
+    assert defs["MAPLE_OBJ_TABLE"] == maple.OBJ_TABLE
+    assert defs["MAPLE_STATUS_NO_FEASIBLE"] == maple.STATUS_NO_FEASIBLE
+
+
 def test_binding_fails_loudly_without_library(tmp_path):
     from paper_2412_13576_b200 import maple as M
     saved = M._lib
