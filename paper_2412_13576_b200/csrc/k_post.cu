@@ -501,7 +501,7 @@ __global__ void bin_scatter_kernel(FilterWork fw, const unsigned long long* dcou
 }
 
 #ifndef MAPLE_IDX_UNROLL
-#define MAPLE_IDX_UNROLL 1
+#define MAPLE_IDX_UNROLL 4
 #endif
 // warp per row g: scan the lists of g's support coordinates (lanes stride each range), stop at the first
 // dominator found by any lane
