@@ -202,6 +202,14 @@ int64_t maple_kernel_launches(const maple_ctx* ctx);
  * descriptors as the descent kernel; the caller compares with an exact host product. */
 int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1, const float* A2, const float* B2,
                         float* D2);
+/* CTA-pair tcgen05 self-test on `device` (host buffers) for the large-shape descent kernel: a cluster of two CTAs,
+ * each holding 64 rows of A; D1 = Ah Bh^T with kind::f16 (Ah 128x32, Bh 160x32, IEEE half bit patterns, fp32 D)
+ * and D2 = A8 B8^T with kind::i8 (A8 128x64, B8 128x64, s32 D), B operands loaded by 3-D TMA boxes into the
+ * canonical SWIZZLE_NONE layout, N split across the pair. raw1 (2 x 128 x 80 fp32) and raw2 (2 x 128 x 64 int32)
+ * receive each CTA's TMEM lanes x columns as read back with tcgen05.ld 32x32b; the caller checks the layout
+ * (row m of CTA r at lane m + 64 (n >= N/2), column n mod N/2) against an exact host product. */
+int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, const int8_t* A8, const int8_t* B8,
+                        float* raw1, int32_t* raw2);
 /* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05 with 2 threads per
  * start, 3 = tcgen05 with 4 threads per start (2 and 3 compute the same iterates). */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);

@@ -16,7 +16,7 @@ BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH
-CU_SOURCES = ["capi.cu", "k_descent_simt.cu", "k_descent_tc.cu", "k_descent_tc4.cu", "k_post.cu", "k_augment.cu", "k_feasible.cu"]
+CU_SOURCES = ["capi.cu", "k_descent_simt.cu", "k_descent_tc.cu", "k_descent_tc4.cu", "k_descent_tcp.cu", "k_post.cu", "k_augment.cu", "k_feasible.cu"]
 CPP_SOURCES = ["lattice.cpp", "sparse_ell.cpp"]
 
 

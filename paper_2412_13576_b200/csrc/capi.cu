@@ -746,6 +746,29 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
     return MAPLE_OK;
 }
 
+int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, const int8_t* A8, const int8_t* B8,
+                        float* raw1, int32_t* raw2) {
+    maple_ctx* ctx = nullptr;
+    if (!Ah || !Bh || !A8 || !B8 || !raw1 || !raw2) return MAPLE_ERR_BAD_ARG;
+    CU(cudaSetDevice(device));
+    g_alloc_stream = 0;
+    const size_t sz[6] = {128 * 32 * 2, 160 * 32 * 2, 128 * 64, 128 * 64, 2 * 128 * 80 * 4, 2 * 128 * 64 * 4};
+    DevBuf b[6];
+    for (int i = 0; i < 6; ++i) CU(b[i].ensure(sz[i]));
+    CU(cudaMemcpy(b[0].p, Ah, sz[0], cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[1].p, Bh, sz[1], cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[2].p, A8, sz[2], cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(b[3].p, B8, sz[3], cudaMemcpyHostToDevice));
+    CU(cudaMemset(b[4].p, 0xFF, sz[4]));
+    CU(cudaMemset(b[5].p, 0xFF, sz[5]));
+    CU(pair_selftest(b[0].p, b[1].p, b[2].p, b[3].p, b[4].as<float>(), b[5].as<int32_t>(), 0));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(raw1, b[4].p, sz[4], cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(raw2, b[5].p, sz[5], cudaMemcpyDeviceToHost));
+    for (auto& x : b) x.release();
+    return MAPLE_OK;
+}
+
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
     if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;

@@ -61,6 +61,10 @@ bool descent_tc_supported(int n, int d);
 cudaError_t umma_selftest(const float* A1, const float* B1, float* D1, const float* A2, const float* B2, float* D2,
                           cudaStream_t s);
 
+// CTA-pair (cta_group::2) self-test (k_descent_tcp.cu): device pointers; see maple_selftest_pair
+cudaError_t pair_selftest(const void* Ah, const void* Bh, const void* A8, const void* B8, float* raw1, int32_t* raw2,
+                          cudaStream_t s);
+
 struct HashSet {
     unsigned long long* keys;     // 0 = empty; else (32-bit hash | 1) << 32 | ref (k_post.cu dedupe_kernel)
     int64_t* newslot;             // per pool index: table slot of a row inserted by the running launch, else -1

@@ -66,6 +66,7 @@ _SIGS = [
     ("maple_set_filter_algorithm", C.c_int, [_P, C.c_int32]),
     ("maple_set_descent_variant", C.c_int, [_P, C.c_int32, C.c_int32]),
     ("maple_selftest_umma", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
+    ("maple_selftest_pair", C.c_int, [C.c_int, _P, _P, _P, _P, _P, _P]),
     ("maple_feasible_starts", C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, _P,
                                         C.c_int32, _P, _P]),
 ]
@@ -131,6 +132,21 @@ def maple_selftest_umma(A1, B1, A2, B2, device=0):
     if rc != 0:
         raise MapleError(rc, "maple_selftest_umma")
     return D1, D2
+
+
+def maple_selftest_pair(Ah, Bh, A8, B8, device=0):
+    """CTA-pair tcgen05 products (f16 and i8, TMA-loaded B split across the pair): raw TMEM read-backs
+    raw1 (2, 128, 80) fp32 and raw2 (2, 128, 64) int32 of each CTA (lanes x columns)."""
+    load()
+    Ah = np.ascontiguousarray(Ah, dtype=np.float16).view(np.uint16)
+    Bh = np.ascontiguousarray(Bh, dtype=np.float16).view(np.uint16)
+    A8, B8 = (np.ascontiguousarray(x, dtype=np.int8) for x in (A8, B8))
+    raw1 = np.zeros((2, 128, 80), np.float32)
+    raw2 = np.zeros((2, 128, 64), np.int32)
+    rc = _lib.maple_selftest_pair(device, _ptr(Ah), _ptr(Bh), _ptr(A8), _ptr(B8), _ptr(raw1), _ptr(raw2))
+    if rc != 0:
+        raise MapleError(rc, "maple_selftest_pair")
+    return raw1, raw2
 
 
 class DirSet:

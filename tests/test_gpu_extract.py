@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from oracle import extraction as OX
+from oracle import lattice as OL
 from oracle import graver as OG
 from oracle import postprocess as OP
 
@@ -46,7 +47,7 @@ def test_basis_and_starts_match_oracle(gpu_lib, name):
     B, Bp = gpu_lib.maple_kernel_basis(inst.A)
     np.testing.assert_array_equal(ctx.B, B)
     Z, Z0 = ctx.debug_descent(4096, 100, 612, 1, 0.01, 7)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, 7, np.arange(100, 612))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), 7, np.arange(100, 612))
     np.testing.assert_allclose(Z0, z0, rtol=1e-12, atol=1e-12)     # fp64 on both sides
 
 
@@ -58,7 +59,7 @@ def test_descent_iterates_small_T_all_starts(gpu_lib, name, T, kernel):
     ctx = _ctx(gpu_lib, inst, kernel)
     N = 1000 if name == "C1" else 1000
     Z, _ = ctx.debug_descent(N, 0, N, T, inst.lr, 11)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, 11, np.arange(N))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), 11, np.arange(N))
     Zo = OX.descend(z0, ctx.B, T, inst.lr)
     assert _pass_frac(Z, Zo) >= 0.999
 
@@ -73,7 +74,7 @@ def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
     ctx = _ctx(gpu_lib, inst, kernel)
     N = 1024
     Z, _ = ctx.debug_descent(N, 0, N, T, inst.lr, inst.seed)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), inst.seed, np.arange(N))
     Z64 = OX.descend(z0, ctx.B, T, inst.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, T, inst.lr, dtype=np.float32)
     gpu, ref = _pass_frac(Z, Z64), _pass_frac(Z32, Z64)
@@ -110,7 +111,7 @@ def test_sets_match_oracle_g3(gpu_lib, name, N, kernel):
     ctx = _ctx(gpu_lib, inst, kernel)
     ds = ctx.extract(N, inst.steps, inst.lr, inst.seed)
     gpu_min = _set(ds.rows())
-    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
+    pool, _ = OX.extract_pool(ctx.B, OL.pinv(ctx.B), inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
     ora_min = OP.minimal_filter(pool)
     j = _jaccard(gpu_min, ora_min)
     print(f"{name} kernel={kernel}: |gpu|={len(gpu_min)} |oracle|={len(ora_min)} jaccard={j:.4f}")
@@ -284,7 +285,7 @@ def test_descent_variants_iterates(gpu_lib, name, kernel, opt):
     ctx = _ctx(gpu_lib, inst, kernel)
     ctx.set_descent_variant(opt)
     N = 1000 if name != "C3" else 128
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), inst.seed, np.arange(N))
     Z, _ = ctx.debug_descent(N, 0, N, 5, inst.lr, inst.seed)
     assert _pass_frac(Z, OX.descend(z0, ctx.B, 5, inst.lr, optimizer=opt)) >= 0.999
     Z, _ = ctx.debug_descent(N, 0, N, 50, inst.lr, inst.seed)

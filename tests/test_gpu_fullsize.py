@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 
 from oracle import extraction as OX
+from oracle import lattice as OL
 from oracle import graver as OG
 from oracle import postprocess as OP
 
@@ -54,7 +55,7 @@ def test_c2a_full_sampled_starts_vs_oracle(gpu_lib):
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
     S_ = 512
     Z, _ = ctx.debug_descent(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(S_))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), inst.seed, np.arange(S_))
     Z64 = OX.descend(z0, ctx.B, inst.steps, inst.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, inst.steps, inst.lr, dtype=np.float32)
 
@@ -62,7 +63,7 @@ def test_c2a_full_sampled_starts_vs_oracle(gpu_lib):
         return float(np.mean(np.all(np.abs(A.astype(np.float64) - R) / np.maximum(1, np.abs(R)) <= 1e-4, axis=1)))
     assert pf(Z, Z64) >= pf(Z32, Z64) - 0.02
     part = _set(ctx.extract_range(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed).rows())
-    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
+    pool, _ = OX.extract_pool(ctx.B, OL.pinv(ctx.B), inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
                               starts=np.arange(S_))
     ora = OP.minimal_filter(pool)
     j = len(part & ora) / max(1, len(part | ora))
@@ -109,7 +110,7 @@ def test_large_configs_small_sizes(gpu_lib, name, N, T):
     assert ctx.descent_kernel == "simt"
     assert np.all(inst.A @ ctx.B == 0)
     Z, _ = ctx.debug_descent(N, 0, N, 3, inst.lr, inst.seed)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(N))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), inst.seed, np.arange(N))
     Zo = OX.descend(z0, ctx.B, 3, inst.lr)
     assert float(np.mean(np.all(np.abs(Z - Zo) / np.maximum(1, np.abs(Zo)) <= 1e-4, axis=1))) >= 0.99
     ctx.set_debug(True)
@@ -129,7 +130,7 @@ def test_c3_directions_vs_oracle(gpu_lib):
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
     rows = ctx.extract(N, inst.steps, inst.lr, inst.seed).rows()
     assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
-    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
+    pool, _ = OX.extract_pool(ctx.B, OL.pinv(ctx.B), inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
     ref, _ = OP.postprocess(inst.A, inst.l, inst.u, np.array(sorted(pool), dtype=np.int64).reshape(-1, inst.n))
     G, R = _set(rows), set(ref)
     assert len(G & R) >= 0.9 * len(G | R)
@@ -168,7 +169,7 @@ def test_c3_full_size_bench_configuration(gpu_lib):
     # sampled starts of the same launch: iterates (G2) and sets (G3)
     S_ = 256
     Z, _ = ctx.debug_descent(inst.n_starts, 0, S_, inst.steps, inst.lr, inst.seed)
-    _, z0 = OX.sample_starts(inst.l, inst.u, ctx.Bp, inst.seed, np.arange(S_))
+    _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), inst.seed, np.arange(S_))
     Z64 = OX.descend(z0, ctx.B, inst.steps, inst.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, inst.steps, inst.lr, dtype=np.float32)
 
@@ -176,7 +177,7 @@ def test_c3_full_size_bench_configuration(gpu_lib):
         return float(np.mean(np.all(np.abs(A.astype(np.float64) - R) / np.maximum(1, np.abs(R)) <= 1e-4, axis=1)))
     assert pf(Z, Z64) >= pf(Z32, Z64) - 0.02
     part = _set(ctx.extract_range(inst.n_starts, 0, 512, inst.steps, inst.lr, inst.seed).rows())
-    pool, _ = OX.extract_pool(ctx.B, ctx.Bp, inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
+    pool, _ = OX.extract_pool(ctx.B, OL.pinv(ctx.B), inst.l, inst.u, inst.n_starts, inst.steps, inst.lr, inst.seed,
                               starts=np.arange(512))
     ref, _ = OP.postprocess(inst.A, inst.l, inst.u, np.array(sorted(pool), dtype=np.int64).reshape(-1, inst.n))
     R = set(ref)
