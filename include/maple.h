@@ -193,6 +193,9 @@ int maple_augment_many(maple_ctx* ctx, const maple_dirset* ds, int32_t n_inst, c
 int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t end, int32_t steps,
                         double step_size, uint64_t seed, float* Z_out, double* Z0_out);
 int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates);
+/* Debug timeline of the CTA-pair descent kernel: enable != 0 arms it for the next launches (cleared); host_out (if not
+ * NULL) receives 2 x 16 x 16 uint64 %globaltimer stamps [cta][step][slot] of the first pair's steps 0..15. */
+int maple_debug_trace(maple_ctx* ctx, int32_t enable, uint64_t* host_out);
 int64_t maple_debug_candidates(maple_ctx* ctx, int32_t* host_rows, int64_t cap);
 int maple_last_timings(const maple_ctx* ctx, float* extract_ms6, float* augment_ms3);
 /* Number of CUDA kernel launches the library issued since the context was created. */
@@ -210,10 +213,13 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
  * (row m of CTA r at lane m + 64 (n >= N/2), column n mod N/2) against an exact host product. */
 int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, const int8_t* A8, const int8_t* B8,
                         float* raw1, int32_t* raw2);
-/* Select the descent kernel: 0 = auto (tcgen05 when the shape fits), 1 = SIMT, 2 = tcgen05 with 2 threads per
- * start, 3 = tcgen05 with 4 threads per start (2 and 3 compute the same iterates). */
+/* Select the descent kernel: 0 = auto (tcgen05 when the shape fits, else the CTA-pair tcgen05 kernel when its shape
+ * fits, else SIMT), 1 = SIMT, 2 = tcgen05 with 2 threads per start, 3 = tcgen05 with 4 threads per start (2 and 3
+ * compute the same iterates), 4 = CTA-pair tcgen05 (large shapes, e.g. n = 300, d = 280: z in TMEM, B streamed by
+ * TMA; Adam with every-step harvest only — a variant or an iterate beyond its f16 operand range runs SIMT). */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
-/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05;
+/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05,
+ * 4 = CTA-pair tcgen05;
  * negative error code for a null context. Host only. */
 int maple_descent_kernel(const maple_ctx* ctx);
 /* Descent variants (DESIGN readings #24-#25). Alg. 3 line 8 updates z with "first-order

@@ -1,6 +1,7 @@
 // C ABI of the MAPLE hot path (include/maple.h): context, extraction pipeline, merge, augmentation.
 // Host code here only orchestrates: every step of the path runs in the kernels of k_*.cu; the host
 // does the once-per-A exact lattice work of maple_create (lattice.cpp) and argument validation.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -110,6 +111,12 @@ struct maple_ctx {
     int filter_minimal = 1;
     int descent_kernel = 0;
     bool sb_ready = false;        // SIMT schedules built (build_sparse)
+    DevBuf B16p, BT8p;            // CTA-pair kernel operands: B (f16, tcp_np x tcp_dp), B^T (int8, tcp_dp x tcp_np)
+    int tcp_np = 0, tcp_dp = 0;   // padded shape of the CTA-pair kernel (0: the shape has none)
+    bool tcp_ready = false;       // B16p / BT8p built (build_tcp)
+    bool tcp_range_fail = false;  // an extraction saw an iterate beyond the f16 operand range: use SIMT from now on
+    DevBuf trace;                 // debug timeline of the CTA-pair kernel (maple_debug_trace)
+    bool trace_on = false;
     int filter_algo = 0;          // 0 auto (indexed), 1 tiled, 2 indexed
     int optimizer = 0;            // reading #24: 0 Adam, 1 GD, 2 sign-GD
     int harvest_final = 0;        // reading #25: 1 = harvest the final iterate only
@@ -144,7 +151,7 @@ struct maple_dirset {
 };
 
 // counters layout in ctx->counters: [0] cand_count, [1] pool_count, [2] n_bad, [3] n_keep, [4] overflow(int)
-enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_NZMAX = 6, C_N = 7 };
+enum { C_CAND = 0, C_POOL = 1, C_BAD = 2, C_KEEP = 3, C_OVF = 4, C_MAXC = 5, C_NZMAX = 6, C_RANGE = 7, C_N = 8 };
 
 #define FAIL(code, msg)              \
     do {                             \
@@ -284,6 +291,10 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
     unsigned long long h[C_N];
     int rc = read_counters(ctx, h);
     if (rc) return rc;
+    if (h[C_RANGE]) {   // the CTA-pair kernel's f16 operands overflowed (|z| > 60000): redo this extraction on SIMT
+        ctx->tcp_range_fail = true;
+        return RETRY;
+    }
     if (h[C_OVF] || (int64_t)h[C_MAXC] > ctx->cand_cap) {
         ctx->want_cand = std::max<int64_t>(ctx->cand_cap, (int64_t)h[C_MAXC] + ((int64_t)h[C_MAXC] >> 2) + 1024);
         ctx->want_pool = h[C_OVF] ? 2 * ctx->pool_cap : ctx->pool_cap;
@@ -404,6 +415,12 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.opt = ctx->optimizer;
     p.harvest_final = ctx->harvest_final;
     p.lr = (float)ctx->tab_lr;   // the step table was just built for this call's step size
+    p.tcp_np = ctx->tcp_np;
+    p.tcp_dp = ctx->tcp_dp;
+    p.B16p = ctx->B16p.as<uint16_t>();
+    p.BT8p = ctx->BT8p.as<int8_t>();
+    p.range_flag = reinterpret_cast<int*>(counters(ctx) + C_RANGE);
+    p.trace = ctx->trace_on ? ctx->trace.as<unsigned long long>() : nullptr;
     return p;
 }
 
@@ -490,12 +507,48 @@ int build_sparse(maple_ctx* ctx) {
 
 constexpr int kAutoTc = 2;   // auto choice for tensor-core shapes
 
-// the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start)
+// Padded operand copies for the CTA-pair kernel (k_descent_tcp.cu): B as IEEE half (exact small integers),
+// tcp_np x tcp_dp, and B^T as int8, tcp_dp x tcp_np, zero padded; uploaded on the context's stream.
+int build_tcp(maple_ctx* ctx) {
+    const int n = ctx->n, d = ctx->d, np = ctx->tcp_np, dp = ctx->tcp_dp;
+    std::vector<uint16_t> b16((size_t)np * dp, 0);
+    std::vector<int8_t> bt8((size_t)dp * np, 0);
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < d; ++j) {
+            const int v = (int)ctx->B[(size_t)i * d + j];
+            b16[(size_t)i * dp + j] = __half_as_ushort(__float2half_rn((float)v));
+            bt8[(size_t)j * np + i] = (int8_t)v;
+        }
+    CU(upload(ctx->B16p, b16));
+    CU(upload(ctx->BT8p, bt8));
+    CU(cudaStreamSynchronize(g_alloc_stream));
+    t_upload_stage.used = 0;
+    ctx->tcp_ready = true;
+    return MAPLE_OK;
+}
+
+// the CTA-pair kernel runs Adam with every-step harvest (the default variant) on the shapes it was instantiated for
+bool tcp_ok(const maple_ctx* ctx) {
+    return ctx->tcp_np > 0 && ctx->optimizer == 0 && ctx->harvest_final == 0 && !ctx->tcp_range_fail;
+}
+
+// the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start),
+// 4 CTA-pair tcgen05 (large shapes)
 int which_descent(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
     const bool variant = ctx->optimizer != 0 || ctx->harvest_final != 0;
+    if (ctx->descent_kernel == 4) return tcp_ok(ctx) ? 4 : 1;
     if (ctx->descent_kernel != 0) return (ctx->descent_kernel == 3 && variant) ? 2 : ctx->descent_kernel;
-    return tc_ok ? kAutoTc : 1;
+    if (tc_ok) return kAutoTc;
+    return tcp_ok(ctx) ? 4 : 1;
+}
+
+// build the schedules / operand copies of the kernel the next launch uses (once per context)
+int ensure_descent_operands(maple_ctx* ctx) {
+    const int w = which_descent(ctx);
+    if (w == 1 && !ctx->sb_ready) return build_sparse(ctx);
+    if (w == 4 && !ctx->tcp_ready) return build_tcp(ctx);
+    return MAPLE_OK;
 }
 
 cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
@@ -503,6 +556,7 @@ cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
     switch (which_descent(ctx)) {
         case 2: return launch_descent_tc(p, ctx->stream);
         case 3: return launch_descent_tc4(p, ctx->stream);
+        case 4: return launch_descent_tcp(p, ctx->stream);
         default: return launch_descent_simt(p, ctx->stream);
     }
 }
@@ -513,8 +567,11 @@ int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t 
     if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
     if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
     if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
-    if (ctx->descent_kernel >= 2 && !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
+    if ((ctx->descent_kernel == 2 || ctx->descent_kernel == 3) &&
+        !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
         FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
+    if (ctx->descent_kernel == 4 && ctx->tcp_np == 0)
+        FAIL(MAPLE_ERR_RANGE, "CTA-pair tcgen05 descent kernel does not support this (n, d)");
     return MAPLE_OK;
 }
 
@@ -648,8 +705,9 @@ int maple_create(const int32_t* A, int32_t m, int32_t n, const int32_t* l, const
     CU(upload(ctx->dBp, ctx->Bp));
     // the SIMT schedules are built now only when the SIMT kernel is the automatic choice; a tcgen05-shaped
     // context builds them on its first SIMT launch (maple_set_descent_kernel(1))
-    if (!(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0)) {
-        const int rc = build_sparse(ctx);
+    tcp_shape(ctx->n, ctx->d, &ctx->tcp_np, &ctx->tcp_dp);
+    {
+        const int rc = ensure_descent_operands(ctx);
         if (rc) return rc;
     }
     CU(upload(ctx->th_off, toff));
@@ -686,7 +744,7 @@ void maple_destroy(maple_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     g_alloc_stream = ctx->stream;
-    DevBuf* bufs[] = {&ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
+    DevBuf* bufs[] = {&ctx->trace, &ctx->B16p, &ctx->BT8p, &ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
                       &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->ell_pos_z, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
@@ -702,6 +760,7 @@ void maple_destroy(maple_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;
+    g_alloc_stream = 0;   // the caller may destroy that stream next; later DevBuf users start from the legacy stream
 }
 
 int maple_set_stream(maple_ctx* ctx, void* stream) {
@@ -730,6 +789,7 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
     maple_ctx* ctx = nullptr;
     if (!A1 || !B1 || !D1 || !A2 || !B2 || !D2) return MAPLE_ERR_BAD_ARG;
     CU(cudaSetDevice(device));
+    g_alloc_stream = 0;
     const size_t sz[6] = {128 * 48, 64 * 48, 128 * 64, 128 * 64, 48 * 64, 128 * 48};
     DevBuf b[6];
     for (int i = 0; i < 6; ++i) CU(b[i].ensure(sz[i] * 4));
@@ -770,7 +830,7 @@ int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, cons
 }
 
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
-    if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
+    if (!ctx || which < 0 || which > 4) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
     return MAPLE_OK;
 }
@@ -791,6 +851,21 @@ int maple_set_filter_algorithm(maple_ctx* ctx, int32_t which) {
 int maple_descent_kernel(const maple_ctx* ctx) {
     if (!ctx) return MAPLE_ERR_BAD_ARG;
     return which_descent(ctx);
+}
+
+int maple_debug_trace(maple_ctx* ctx, int32_t enable, uint64_t* host_out) {
+    if (!ctx) return MAPLE_ERR_BAD_ARG;
+    g_alloc_stream = ctx->stream;
+    if (enable) {
+        CU(ctx->trace.ensure(2 * 16 * 16 * 8));
+        CU(cudaMemsetAsync(ctx->trace.p, 0, 2 * 16 * 16 * 8, ctx->stream));
+    }
+    ctx->trace_on = enable != 0;
+    if (host_out && ctx->trace.p) {
+        CU(cudaMemcpyAsync(host_out, ctx->trace.p, 2 * 16 * 16 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+    }
+    return MAPLE_OK;
 }
 
 int maple_set_debug(maple_ctx* ctx, int32_t keep_candidates) {
@@ -867,10 +942,8 @@ int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
         for (int64_t c0 = begin; c0 < end; c0 += chunk_max) {
             const int64_t cnt = std::min(chunk_max, end - c0);
             CU(cudaMemsetAsync(counters(ctx) + C_CAND, 0, 8, s));
-            if (which_descent(ctx) == 1 && !ctx->sb_ready) {
-                rc = build_sparse(ctx);
-                if (rc) return rc;
-            }
+            rc = ensure_descent_operands(ctx);
+            if (rc) return rc;
             DescentParams p = descent_params(ctx, steps, seed, n_starts, c0, cnt);
             p.harvest = 1;
             p.cand = ctx->cand.as<int8_t>();
@@ -1009,10 +1082,8 @@ int maple_debug_descent(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
     if (cnt == 0) return MAPLE_OK;
     CU(ctx->zout.ensure((size_t)cnt * ctx->d * sizeof(float)));
     CU(ctx->z0out.ensure((size_t)cnt * ctx->d * sizeof(double)));
-    if (which_descent(ctx) == 1 && !ctx->sb_ready) {
-        rc = build_sparse(ctx);
-        if (rc) return rc;
-    }
+    rc = ensure_descent_operands(ctx);
+    if (rc) return rc;
     DescentParams p = descent_params(ctx, steps, seed, n_starts, begin, cnt);
     p.harvest = 0;
     p.Z_out = ctx->zout.as<float>();

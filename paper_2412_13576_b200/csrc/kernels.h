@@ -48,6 +48,12 @@ struct DescentParams {
     unsigned long long* cand_count;
     float* Z_out;                 // optional: final iterates (count x d)
     double* Z0_out;               // optional: starts (count x d)
+    // CTA-pair tcgen05 kernel (k_descent_tcp.cu): padded operand copies of B and the range flag
+    int tcp_np, tcp_dp;           // padded n (multiple of 64) and d (multiple of 96 / 32, see tcp_shape)
+    const uint16_t* B16p;         // B as IEEE half, tcp_np x tcp_dp row-major (zero padded)
+    const int8_t* BT8p;           // B^T as int8, tcp_dp x tcp_np row-major (zero padded)
+    int* range_flag;              // set to 1 if an iterate left the f16 range of the operands (|z| > 60000)
+    unsigned long long* trace;    // optional (debug): per-step %globaltimer stamps of the first pair (tcp kernel)
 };
 
 // SIMT descent + harvest (one warp per start). Returns a cudaError_t.
@@ -61,6 +67,10 @@ bool descent_tc_supported(int n, int d);
 cudaError_t umma_selftest(const float* A1, const float* B1, float* D1, const float* A2, const float* B2, float* D2,
                           cudaStream_t s);
 
+// CTA-pair tcgen05 descent + harvest (64 starts per CTA, 128 per pair; state on chip: z in TMEM, Adam m / v in
+// registers). tcp_shape: the padded (np, dp) a shape runs at, false when no instantiation fits.
+bool tcp_shape(int n, int d, int* np, int* dp);
+cudaError_t launch_descent_tcp(const DescentParams& p, cudaStream_t s);
 // CTA-pair (cta_group::2) self-test (k_descent_tcp.cu): device pointers; see maple_selftest_pair
 cudaError_t pair_selftest(const void* Ah, const void* Bh, const void* A8, const void* B8, float* raw1, int32_t* raw2,
                           cudaStream_t s);

@@ -45,6 +45,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t saddr, uint32_t b
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr), "r"(bytes) : "memory");
 }
 
+// Waits sleep in hardware for at most 20 us per probe; a phase that never completes traps after about 2^20
+// probes (~20 s), so a protocol bug ends the kernel with an error instead of hanging the device.
 // wait with cluster-scope acquire (for barriers whose arrivals come from the peer CTA's threads)
 __device__ __forceinline__ bool mbar_try_cluster(uint32_t a, uint32_t parity) {
     uint32_t ok;
@@ -53,20 +55,31 @@ __device__ __forceinline__ bool mbar_try_cluster(uint32_t a, uint32_t parity) {
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, P1;\n\t}\n"
         : "=r"(ok)
-        : "r"(a), "r"(parity), "r"(0x989680u)
+        : "r"(a), "r"(parity), "r"(20000u)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try_local(uint32_t a, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(20000u)
         : "memory");
     return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
     uint32_t spins = 0;
     while (!mbar_try_cluster(a, parity)) {
-        if (++spins > (1u << 22)) asm volatile("trap;");
+        if (++spins > (1u << 20)) asm volatile("trap;");
     }
 }
 __device__ __forceinline__ void mbar_wait_local(uint32_t a, uint32_t parity) {
     uint32_t spins = 0;
-    while (!umma::mbar_try(a, parity)) {
-        if (++spins > (1u << 22)) asm volatile("trap;");
+    while (!mbar_try_local(a, parity)) {
+        if (++spins > (1u << 20)) asm volatile("trap;");
     }
 }
 

@@ -58,6 +58,7 @@ _SIGS = [
     ("maple_augment_many", C.c_int, [_P, _P, C.c_int32, C.POINTER(maple_objective), _P, _P, C.c_int32, _P, _P]),
     ("maple_debug_descent", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_uint64, _P, _P]),
     ("maple_set_debug", C.c_int, [_P, C.c_int32]),
+    ("maple_debug_trace", C.c_int, [_P, C.c_int32, _P]),
     ("maple_debug_candidates", C.c_int64, [_P, _P, C.c_int64]),
     ("maple_last_timings", C.c_int, [_P, _P, _P]),
     ("maple_kernel_launches", C.c_int64, [_P]),
@@ -247,10 +248,17 @@ class Context:
 
     @property
     def descent_kernel(self) -> str:
-        """'simt', 'tc' or 'tc4': the descent kernel the next extraction launches."""
+        """'simt', 'tc', 'tc4' or 'tcp' (CTA-pair tcgen05, large shapes): the descent kernel the next extraction
+        launches."""
         r = _lib.maple_descent_kernel(self.h)
         _check(min(r, 0), self.h)
-        return {1: "simt", 2: "tc", 3: "tc4"}[r]
+        return {1: "simt", 2: "tc", 3: "tc4", 4: "tcp"}[r]
+
+    def debug_trace(self, enable: bool = True):
+        """Arm (enable) or read back the CTA-pair kernel's per-step timeline: (2, 16, 16) uint64 ns stamps."""
+        out = np.zeros((2, 16, 16), np.uint64)
+        _check(_lib.maple_debug_trace(self.h, 1 if enable else 0, _ptr(out)), self.h)
+        return out
 
     def set_debug(self, keep_candidates: bool):
         _check(_lib.maple_set_debug(self.h, int(keep_candidates)), self.h)

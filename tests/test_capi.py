@@ -86,19 +86,59 @@ def test_library_basis_random(maple, seed):
     assert L.is_lll_reduced(B.tolist())
 
 
-def test_library_basis_c3_shape(maple):
-    from synth import c3
-    inst = c3()
-    B, _ = maple.maple_kernel_basis(inst.A)
-    assert B.shape == (300, 280)
-    assert np.all(inst.A @ B == 0)
-    # fp64 reducedness check with tolerance, d = 280
-    Bf = B.astype(np.float64)
-    Qm, R = np.linalg.qr(Bf)
+def _free_columns(A):
+    """A = [I_m | W] Pi (synth identity-block recipe): one unit column e_r per row r is an identity column; the
+    other d columns F are the free coordinates, and x -> x_F maps Ker_Z(A) bijectively onto Z^d (x_I = -W x_F)."""
+    m, n = A.shape
+    ident = []
+    for r in range(m):
+        ident.append(next(k for k in range(n) if A[r, k] == 1 and np.count_nonzero(A[:, k]) == 1))
+    return np.array([k for k in range(n) if k not in set(ident)])
+
+
+def _unimodular(M):
+    """|det M| = 1 for a square integer M, certified exactly: X = round(inv(M)) and M X = I in exact int64
+    arithmetic (entries bounded first) give det(M) det(X) = 1 with both determinants integers."""
+    X = np.rint(np.linalg.inv(M.astype(np.float64)))
+    if not np.all(np.isfinite(X)) or np.abs(X).max() >= 2.0 ** 40 / M.shape[0] / max(1, np.abs(M).max()):
+        return False
+    P = M.astype(np.int64) @ X.astype(np.int64)
+    return np.array_equal(P, np.eye(M.shape[0], dtype=np.int64))
+
+
+def _reduced_fp64(B, tol=1e-9):
+    """Def. 'reduced basis' in fp64 with SPEC S:83's tolerance: |mu_ij| <= 1/2 + tol and
+    ||B*_j||^2 <= 2 ||B*_{j+1}||^2 (1 + tol), the GSO from a Householder QR (|R_jj| = ||B*_j||, mu = R / R_jj).
+    For these integer bases (|B| <= 3, d <= 900) the QR's backward error is ~1e-13 relative, far inside tol."""
+    R = np.linalg.qr(B.astype(np.float64), mode="r")
     diag = np.abs(np.diag(R))
     mu = R / np.where(diag == 0, 1, diag)[:, None]
-    assert np.all(np.abs(np.triu(mu, 1)) <= 0.5 + 1e-9)
-    assert np.all(diag[:-1] ** 2 <= 2 * diag[1:] ** 2 * (1 + 1e-9))
+    return bool(np.all(np.abs(np.triu(mu, 1)) <= 0.5 + tol) and np.all(diag[:-1] ** 2 <= 2 * diag[1:] ** 2 * (1 + tol)))
+
+
+@pytest.mark.parametrize("name,shape", [("C3", (300, 280)), ("C5", (1000, 900))])
+def test_library_basis_large_saturated_and_reduced(maple, name, shape):
+    """configs[2] / configs[4] shapes: Thm. 1 exactly — A B = 0 and L(B) = Ker_Z(A), the latter as
+    unimodularity of B restricted to the free coordinates (an exact integer certificate) — and LLL-reducedness
+    (Def. P:136-144) in fp64 at SPEC S:83's tolerance."""
+    from synth import config
+    inst = config(name)
+    B, Bp = maple.maple_kernel_basis(inst.A)
+    assert B.shape == shape
+    assert np.all(inst.A.astype(np.int64) @ B.astype(np.int64) == 0)
+    F = _free_columns(inst.A)
+    assert len(F) == shape[1]
+    assert _unimodular(B[F, :])
+    assert _reduced_fp64(B)
+    np.testing.assert_allclose(Bp, L.pinv(B), rtol=1e-9, atol=1e-12)
+
+
+def test_unimodular_certificate_rejects():
+    """The saturation certificate is not vacuous: a basis of an index-2 sublattice fails it."""
+    M = np.eye(5, dtype=np.int64)
+    M[2, 2] = 2
+    assert not _unimodular(M)
+    assert _unimodular(np.array([[2, 1], [1, 1]]))
 
 
 def test_create_errors(maple):

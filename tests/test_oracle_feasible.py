@@ -46,3 +46,36 @@ def test_results_are_exactly_the_feasible_points_found():
          if np.all(inst.A @ np.array(p) == inst.b)}
     assert set(pts) <= S and len(pts) > 0
     assert pts == sorted(pts)
+
+
+def test_projected_adam_matches_torch():
+    """Readings F2-F3 pinned to library routines: the Eq. 4 loss differentiated by torch autograd (not F.grad),
+    stepped by torch.optim.Adam (the paper's optimizer, PyTorch 2.1.0 P:452) and projected with clamp_
+    onto [l, u] after every step, equals feasible.descend in fp64 (a bias-correction, projection-order or
+    gradient slip fails this)."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(12)
+    for trial in range(6):
+        m, n = int(rng.integers(1, 4)), int(rng.integers(3, 7))
+        A = rng.integers(-3, 4, size=(m, n))
+        b = rng.integers(-4, 5, size=m)
+        l = rng.integers(-2, 1, size=n)
+        u = l + rng.integers(1, 4, size=n)
+        X0 = F.starts(l, u, 7 + trial, np.arange(5))
+        steps, lr, lam3 = 40, 0.05, 0.1
+        ref = F.descend(X0, A, b, l, u, steps, lr, lam3=lam3)
+        x = torch.tensor(X0, dtype=torch.float64, requires_grad=True)
+        At = torch.tensor(A, dtype=torch.float64)
+        bt = torch.tensor(b, dtype=torch.float64)
+        lo = torch.tensor(l, dtype=torch.float64)
+        hi = torch.tensor(u, dtype=torch.float64)
+        opt = torch.optim.Adam([x], lr=lr, betas=(0.9, 0.999), eps=1e-8)
+        for _ in range(steps):
+            opt.zero_grad()
+            r = x @ At.T - bt
+            f = (r * r).sum() + lam3 * ((x - torch.floor(x)) * (torch.ceil(x) - x)).sum()
+            f.backward()
+            opt.step()
+            with torch.no_grad():
+                x.clamp_(min=lo, max=hi)
+        np.testing.assert_allclose(x.detach().numpy(), ref, rtol=1e-10, atol=1e-10)

@@ -1,0 +1,23 @@
+"""One C3 extraction with a chosen descent kernel (for ncu captures): python tools/tcp_one.py kernel N T"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    from paper_2412_13576_b200 import maple
+    from synth import c3
+    kernel, N, T = (int(x) for x in sys.argv[1:4])
+    inst = c3()
+    maple.load()
+    ctx = maple.Context(inst.A, inst.l, inst.u)
+    ctx.set_descent_kernel(kernel)
+    ds = ctx.extract(N, T, inst.lr, inst.seed)
+    torch.cuda.synchronize()
+    print(ctx.descent_kernel, N, T, "descent ms", ctx.timings()["descent"], "rows", ds.size)
+
+
+if __name__ == "__main__":
+    main()
