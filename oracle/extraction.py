@@ -109,7 +109,12 @@ def canonicalize_rows(G: np.ndarray) -> np.ndarray:
 def harvest(Z, B, l, u):
     """Alg. 3 lines 9-10 for every row: g = B ⌈z⌋, kept iff g in [l-u, u-l] and g != 0; canonical rows."""
     R = round_half_away(Z)
-    G = R @ np.asarray(B, dtype=np.int64).T
+    Bi = np.asarray(B, dtype=np.int64)
+    # B r exactly: a float64 product of integers is exact while every partial sum stays below 2^53
+    if R.size and np.abs(R).max() * np.abs(Bi).sum(axis=1).max() < 2.0 ** 53:
+        G = (R.astype(np.float64) @ Bi.T.astype(np.float64)).astype(np.int64)
+    else:
+        G = R @ Bi.T
     box = (u - l).astype(np.int64)
     keep = np.all(np.abs(G) <= box[None, :], axis=1) & np.any(G != 0, axis=1)
     return canonicalize_rows(G[keep])

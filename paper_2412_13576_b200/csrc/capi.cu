@@ -111,7 +111,7 @@ struct maple_ctx {
     int filter_minimal = 1;
     int descent_kernel = 0;
     bool sb_ready = false;        // SIMT schedules built (build_sparse)
-    DevBuf B16p, BT8p;            // CTA-pair kernel operands: B (f16, tcp_np x tcp_dp), B^T (int8, tcp_dp x tcp_np)
+    DevBuf B16p, BT8p, B8p;       // CTA-pair kernel operands: B (f16 and int8, tcp_np x tcp_dp), B^T (int8, tcp_dp x tcp_np)
     int tcp_np = 0, tcp_dp = 0;   // padded shape of the CTA-pair kernel (0: the shape has none)
     bool tcp_ready = false;       // B16p / BT8p built (build_tcp)
     bool tcp_range_fail = false;  // an extraction saw an iterate beyond the f16 operand range: use SIMT from now on
@@ -419,6 +419,7 @@ DescentParams descent_params(maple_ctx* ctx, int T, uint64_t seed, int64_t n_tot
     p.tcp_dp = ctx->tcp_dp;
     p.B16p = ctx->B16p.as<uint16_t>();
     p.BT8p = ctx->BT8p.as<int8_t>();
+    p.B8p = ctx->B8p.as<int8_t>();
     p.range_flag = reinterpret_cast<int*>(counters(ctx) + C_RANGE);
     p.trace = ctx->trace_on ? ctx->trace.as<unsigned long long>() : nullptr;
     return p;
@@ -512,15 +513,17 @@ constexpr int kAutoTc = 2;   // auto choice for tensor-core shapes
 int build_tcp(maple_ctx* ctx) {
     const int n = ctx->n, d = ctx->d, np = ctx->tcp_np, dp = ctx->tcp_dp;
     std::vector<uint16_t> b16((size_t)np * dp, 0);
-    std::vector<int8_t> bt8((size_t)dp * np, 0);
+    std::vector<int8_t> bt8((size_t)dp * np, 0), b8((size_t)np * dp, 0);
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < d; ++j) {
             const int v = (int)ctx->B[(size_t)i * d + j];
             b16[(size_t)i * dp + j] = __half_as_ushort(__float2half_rn((float)v));
             bt8[(size_t)j * np + i] = (int8_t)v;
+            b8[(size_t)i * dp + j] = (int8_t)v;
         }
     CU(upload(ctx->B16p, b16));
     CU(upload(ctx->BT8p, bt8));
+    CU(upload(ctx->B8p, b8));
     CU(cudaStreamSynchronize(g_alloc_stream));
     t_upload_stage.used = 0;
     ctx->tcp_ready = true;
@@ -529,7 +532,9 @@ int build_tcp(maple_ctx* ctx) {
 
 // the CTA-pair kernel runs Adam with every-step harvest (the default variant) on the shapes it was instantiated for
 bool tcp_ok(const maple_ctx* ctx) {
-    return ctx->tcp_np > 0 && ctx->optimizer == 0 && ctx->harvest_final == 0 && !ctx->tcp_range_fail;
+    // the harvest operand is round(z) as int8: exact for every in-box g when |B+ g|_inf <= rbound < 127
+    return ctx->tcp_np > 0 && ctx->optimizer == 0 && ctx->harvest_final == 0 && !ctx->tcp_range_fail &&
+           ctx->rbound < 127.0;
 }
 
 // the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start),
@@ -744,7 +749,7 @@ void maple_destroy(maple_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     g_alloc_stream = ctx->stream;
-    DevBuf* bufs[] = {&ctx->trace, &ctx->B16p, &ctx->BT8p, &ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
+    DevBuf* bufs[] = {&ctx->trace, &ctx->B16p, &ctx->BT8p, &ctx->B8p, &ctx->A_rowptr, &ctx->A_col, &ctx->A_val, &ctx->dl, &ctx->du, &ctx->dbox, &ctx->B_nd,
                       &ctx->B_dn, &ctx->B8, &ctx->dBp, &ctx->th_off, &ctx->th_c0, &ctx->th_c1,
                       &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->ell_pos_z, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,

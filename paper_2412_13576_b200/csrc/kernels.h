@@ -52,6 +52,7 @@ struct DescentParams {
     int tcp_np, tcp_dp;           // padded n (multiple of 64) and d (multiple of 96 / 32, see tcp_shape)
     const uint16_t* B16p;         // B as IEEE half, tcp_np x tcp_dp row-major (zero padded)
     const int8_t* BT8p;           // B^T as int8, tcp_dp x tcp_np row-major (zero padded)
+    const int8_t* B8p;            // B as int8, tcp_np x tcp_dp row-major (zero padded; the harvest operand)
     int* range_flag;              // set to 1 if an iterate left the f16 range of the operands (|z| > 60000)
     unsigned long long* trace;    // optional (debug): per-step %globaltimer stamps of the first pair (tcp kernel)
 };

@@ -41,11 +41,13 @@ def _pass_frac(Z, Zref, tol=1e-4):
 
 @pytest.mark.parametrize("name", ["C1", "C2a", "C2b"])
 def test_basis_and_starts_match_oracle(gpu_lib, name):
+    """The context's exported B is a saturated, LLL-reduced kernel basis by the oracle's exact checkers (Thm. 1,
+    Def. P:136-144), and the device starts z0 = B+ g0 equal the oracle's (its own pseudoinverse of that B)."""
     from synth import config
     inst = config(name)
     ctx = _ctx(gpu_lib, inst)
-    B, Bp = gpu_lib.maple_kernel_basis(inst.A)
-    np.testing.assert_array_equal(ctx.B, B)
+    assert OL.is_kernel_basis(inst.A, ctx.B.tolist())
+    assert OL.is_lll_reduced(ctx.B.tolist())
     Z, Z0 = ctx.debug_descent(4096, 100, 612, 1, 0.01, 7)
     _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), 7, np.arange(100, 612))
     np.testing.assert_allclose(Z0, z0, rtol=1e-12, atol=1e-12)     # fp64 on both sides (P:401-402)
@@ -67,7 +69,7 @@ def test_descent_iterates_small_T_all_starts(gpu_lib, name, T, kernel):
 @pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
 @pytest.mark.parametrize("name,T", [("C1", 50), ("C1", 200), ("C2a", 50), ("C2a", 200)])
 def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
-    """pass_frac(GPU vs fp64) >= pass_frac(fp32 oracle vs fp64) - 0.01 (the method is chaotic: even exact
+    """pass_frac(GPU vs fp64) >= pass_frac(fp32 oracle vs fp64) - 0.005 (the method is chaotic: even exact
     fp32 arithmetic loses 1e-4 agreement on some starts)."""
     from synth import config
     inst = config(name)
@@ -79,7 +81,7 @@ def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, T, inst.lr, dtype=np.float32)
     gpu, ref = _pass_frac(Z, Z64), _pass_frac(Z32, Z64)
     print(f"{name} T={T} kernel={kernel}: gpu pass {gpu:.4f}, fp32-oracle pass {ref:.4f}")
-    assert gpu >= ref - 0.01
+    assert gpu >= ref - 0.005
 
 
 @pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
@@ -291,7 +293,7 @@ def test_descent_variants_iterates(gpu_lib, name, kernel, opt):
     Z, _ = ctx.debug_descent(N, 0, N, 50, inst.lr, inst.seed)
     Z64 = OX.descend(z0, ctx.B, 50, inst.lr, optimizer=opt)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, 50, inst.lr, optimizer=opt, dtype=np.float32)
-    assert _pass_frac(Z, Z64) >= _pass_frac(Z32, Z64) - 0.01
+    assert _pass_frac(Z, Z64) >= _pass_frac(Z32, Z64) - 0.005
 
 
 @pytest.mark.parametrize("name,kernel", [("C1", TC), ("C2a", TC), ("C2a", SIMT), ("C2b", TC), ("C3", SIMT)])

@@ -24,10 +24,10 @@ def main():
     torch.cuda.synchronize()
     tr = ctx.debug_trace(False).astype(np.int64)
     names = ["mma:waitA", "mma:A", "mma:fwd", "mma:S", "mma:bwd", "epi:waitG", "epi:G", "epi:sign", "epi:waitM",
-             "epi:M", "epi:adam"]
+             "epi:M", "epi:adam", "epi:H"]
     for cta in range(2):
         for t in (5, 6, 7):
-            row = tr[cta, t, :11]
+            row = tr[cta, t, :12]
             t0 = row[row > 0].min() if np.any(row > 0) else 0
             print(f"cta {cta} step {t}: " + "  ".join(f"{names[k]} {(row[k] - t0) / 1e3:6.2f}" for k in range(11) if row[k]))
         steps = tr[cta, 2:15, 6]
