@@ -139,6 +139,10 @@ int maple_dirset_copy(const maple_dirset* ds, int32_t* host_rows);            /*
 /* Same rows as int8 (every entry lies in [-(u-l), u-l] with u-l <= 127): one strided device-to-host copy of
  * size*n bytes into caller-owned host memory (pageable or pinned), synchronised on the context stream. */
 int maple_dirset_copy_i8(const maple_dirset* ds, int8_t* host_rows);
+/* One contiguous device-to-host copy of the size x stride int8 rows as stored (stride = maple_dirset_stride >= n,
+ * bytes n..stride-1 of a row are 0) into host_rows (size x stride bytes; pinned memory makes it one DMA at link
+ * speed). Enqueued on the context stream and synchronised. */
+int maple_dirset_copy_raw(const maple_dirset* ds, int8_t* host_rows);
 const int8_t* maple_dirset_device_rows(const maple_dirset* ds);   /* borrowed; stride maple_dirset_stride */
 /* Device-to-device copy of the size x stride int8 rows into caller memory `dst` (e.g. a torch tensor that
  * feeds the NCCL all-gather); enqueued on the context stream and synchronised. */
@@ -214,11 +218,10 @@ int maple_selftest_umma(int device, const float* A1, const float* B1, float* D1,
 int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, const int8_t* A8, const int8_t* B8,
                         float* raw1, int32_t* raw2);
 /* Select the descent kernel: 0 = auto (tcgen05 when the shape fits, else the CTA-pair tcgen05 kernel when its shape
- * fits, else SIMT), 1 = SIMT, 2 = tcgen05 with 2 threads per start, 3 = tcgen05 with 4 threads per start (2 and 3
- * compute the same iterates), 4 = CTA-pair tcgen05 (large shapes, e.g. n = 300, d = 280: z in TMEM, B streamed by
+ * fits, else SIMT), 1 = SIMT, 2 = tcgen05 (n, d <= 64; 2 threads per start), 4 = CTA-pair tcgen05 (large shapes, e.g. n = 300, d = 280: z in TMEM, B streamed by
  * TMA; Adam with every-step harvest only — a variant or an iterate beyond its f16 operand range runs SIMT). */
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which);
-/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 / 3 = tcgen05,
+/* The descent kernel the next extraction on `ctx` launches: 1 = SIMT (sparse B, warp per start), 2 = tcgen05,
  * 4 = CTA-pair tcgen05;
  * negative error code for a null context. Host only. */
 int maple_descent_kernel(const maple_ctx* ctx);
@@ -226,8 +229,8 @@ int maple_descent_kernel(const maple_ctx* ctx);
  * methods such as Adam": optimizer 0 = Adam (default, torch.optim.Adam formula), 1 = plain gradient descent
  * z <- z - step_size * g, 2 = sign gradient descent z <- z - step_size * sign(g) (sign(0) = 0), g the Eq. 3
  * subgradient. harvest_final = 1 applies Alg. 3 lines 9-10 to the final iterate z_T only (0: after
- * every step, the paper's loop). The 4-thread tcgen05 kernel implements the default only: a variant extraction
- * with descent kernel 3 selected runs kernel 2. Returns BAD_ARG for a null context or out-of-range values. Host only. */
+ * every step, the paper's loop). The CTA-pair kernel implements the default only: a variant extraction on a context
+ * whose kernel would be 4 runs SIMT. Returns BAD_ARG for a null context or out-of-range values. Host only. */
 int maple_set_descent_variant(maple_ctx* ctx, int32_t optimizer, int32_t harvest_final);
 /* Select the ⊑-minimality filter's pair enumeration (Def. 1-2; the kept set is the same for all):
  * 0 = auto (indexed when n <= 1024), 1 = tiled (every row against all rows of smaller L1 norm), 2 = indexed

@@ -16,7 +16,7 @@ BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v"] + ARCH
-CU_SOURCES = ["capi.cu", "k_descent_simt.cu", "k_descent_tc.cu", "k_descent_tc4.cu", "k_descent_tcp.cu", "k_post.cu", "k_augment.cu", "k_feasible.cu"]
+CU_SOURCES = ["capi.cu", "k_descent_simt.cu", "k_descent_tc.cu", "k_descent_tcp.cu", "k_post.cu", "k_augment.cu", "k_feasible.cu"]
 CPP_SOURCES = ["lattice.cpp", "sparse_ell.cpp"]
 
 
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             if src.endswith(".cu"):
                 jobs.append([NVCC] + NVFLAGS + ["-c", s, "-o", o])
             else:
-                jobs.append(["g++", "-std=c++17", "-O3", "-fPIC", "-c", s, "-o", o])
+                jobs.append(["g++", "-std=c++17", "-O3", "-fPIC", "-pthread", "-c", s, "-o", o])
     logs = []
     with ThreadPoolExecutor(max_workers=max(1, min(8, len(jobs)))) as ex:
         logs = list(ex.map(_run, jobs))

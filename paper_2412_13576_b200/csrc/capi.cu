@@ -203,7 +203,7 @@ int read_counters(maple_ctx* ctx, unsigned long long* h) {
 }
 
 // Size the candidate buffer, the hash set (pool + table) and the per-row work buffers, then reset the set.
-int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
+int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap, int filter_minimal) {
     const int np = ctx->n_pad;
     // the hash set references rows by 31-bit indices (k_post.cu dedupe_kernel)
     if (cand_cap >= (int64_t(1) << 31) || pool_cap >= (int64_t(1) << 31)) return MAPLE_ERR_CAPACITY;
@@ -228,13 +228,15 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap) {
         CU(ctx->witness.ensure(K * 4));
         CU(ctx->order.ensure(K * 4));
         CU(ctx->l1.ensure(K * 4));
-        CU(ctx->codes.ensure((size_t)K * 2 * std::max(ctx->Wh, 1) * 4));
         CU(ctx->sig.ensure((size_t)K * 16));
         CU(ctx->fkey.ensure((size_t)K * 4));
         CU(ctx->flrow.ensure((size_t)K * 4));
         CU(ctx->flsig.ensure((size_t)K * 16));
         CU(ctx->tmp_rows.ensure((size_t)K * np));
     }
+    // thermometer codes only when the ⊑ filter runs (the unfiltered mode accepts Wh > 32, where these would be
+    // K x 2 Wh words); the check kernel writes them only with encode = filter_minimal (ensure() only grows)
+    if (filter_minimal) CU(ctx->codes.ensure((size_t)ctx->pool_cap * 2 * std::max(ctx->Wh, 1) * 4));
     CU(ctx->hist.ensure((size_t)(ctx->Lh + 2) * 4));
     CU(ctx->level_start.ensure((size_t)(ctx->Lh + 2) * 4));
     CU(ctx->cursor.ensure((size_t)(ctx->Lh + 2) * 4));
@@ -344,7 +346,7 @@ int insert_rows_and_finish(maple_ctx* ctx, const int8_t* drows, int64_t k, int s
                            maple_dirset** out) {
     cudaStream_t s = ctx->stream;
     for (int attempt = 0; attempt < 8; ++attempt) {
-        int rc = prepare_set(ctx, std::max<int64_t>(k, 1), std::max<int64_t>({k, ctx->want_pool, 1}));
+        int rc = prepare_set(ctx, std::max<int64_t>(k, 1), std::max<int64_t>({k, ctx->want_pool, 1}), filter_minimal);
         if (rc) return rc;
         CU(cudaEventRecord(ctx->ev[0], s));
         const unsigned long long kk = (unsigned long long)k;
@@ -537,13 +539,13 @@ bool tcp_ok(const maple_ctx* ctx) {
            ctx->rbound < 127.0;
 }
 
-// the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (2 threads / start), 3 tcgen05 (4 threads / start),
-// 4 CTA-pair tcgen05 (large shapes)
+// the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (small shapes), 4 CTA-pair tcgen05 (large shapes)
 int which_descent(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
     const bool variant = ctx->optimizer != 0 || ctx->harvest_final != 0;
     if (ctx->descent_kernel == 4) return tcp_ok(ctx) ? 4 : 1;
-    if (ctx->descent_kernel != 0) return (ctx->descent_kernel == 3 && variant) ? 2 : ctx->descent_kernel;
+    (void)variant;
+    if (ctx->descent_kernel != 0) return ctx->descent_kernel;
     if (tc_ok) return kAutoTc;
     return tcp_ok(ctx) ? 4 : 1;
 }
@@ -560,7 +562,6 @@ cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
     ctx->launches++;
     switch (which_descent(ctx)) {
         case 2: return launch_descent_tc(p, ctx->stream);
-        case 3: return launch_descent_tc4(p, ctx->stream);
         case 4: return launch_descent_tcp(p, ctx->stream);
         default: return launch_descent_simt(p, ctx->stream);
     }
@@ -572,7 +573,7 @@ int check_extract_args(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t 
     if (steps < 1) FAIL(MAPLE_ERR_BAD_ARG, "steps must be >= 1");
     if (!(lr > 0.0) || !std::isfinite(lr)) FAIL(MAPLE_ERR_BAD_ARG, "step_size must be > 0");
     if (begin < 0 || end > n_starts || begin > end) FAIL(MAPLE_ERR_BAD_ARG, "bad start range");
-    if ((ctx->descent_kernel == 2 || ctx->descent_kernel == 3) &&
+    if (ctx->descent_kernel == 2 &&
         !(descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0))
         FAIL(MAPLE_ERR_RANGE, "tcgen05 descent kernel does not support this (n, d)");
     if (ctx->descent_kernel == 4 && ctx->tcp_np == 0)
@@ -835,7 +836,7 @@ int maple_selftest_pair(int device, const uint16_t* Ah, const uint16_t* Bh, cons
 }
 
 int maple_set_descent_kernel(maple_ctx* ctx, int32_t which) {
-    if (!ctx || which < 0 || which > 4) return MAPLE_ERR_BAD_ARG;
+    if (!ctx || which < 0 || which > 4 || which == 3) return MAPLE_ERR_BAD_ARG;
     ctx->descent_kernel = which;
     return MAPLE_OK;
 }
@@ -939,7 +940,7 @@ int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
     for (int attempt = 0; attempt < 8; ++attempt) {
         const int64_t pool_want = std::max<int64_t>(ctx->want_pool, std::max(ctx->want_cand, ctx->cand_cap) *
                                                                          std::min<int64_t>(nchunks, 4));
-        rc = prepare_set(ctx, std::max(ctx->want_cand, ctx->cand_cap), pool_want);
+        rc = prepare_set(ctx, std::max(ctx->want_cand, ctx->cand_cap), pool_want, ctx->filter_minimal);
         if (rc) return rc;
         ctx->dbg_cand.clear();
         ctx->dbg_count = 0;
@@ -1002,9 +1003,10 @@ int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32
             if (v > 127 || v < -127) FAIL(MAPLE_ERR_RANGE, "row entry outside int8");
             h[(size_t)r * np + i] = (int8_t)v;
         }
-    DevBuf tmp;
+    DevBuf tmp;   // stream-ordered on ctx->stream (g_alloc_stream), like the upload and the kernels that read it
     CU(tmp.ensure(h.size()));
-    CU(cudaMemcpy(tmp.p, h.data(), h.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(tmp.p, h.data(), h.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));   // h is pageable and local
     int rc = insert_rows_and_finish(ctx, tmp.as<int8_t>(), k, np, filter_minimal ? 1 : 0, out);
     tmp.release();
     return rc;
@@ -1033,6 +1035,15 @@ int maple_dirset_copy_i8(const maple_dirset* ds, int8_t* host_rows) {
     maple_ctx* ctx = ds->ctx;
     CU(cudaMemcpy2DAsync(host_rows, (size_t)ds->n, ds->rows, (size_t)ds->n_pad, (size_t)ds->n, (size_t)ds->size,
                          cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return MAPLE_OK;
+}
+
+int maple_dirset_copy_raw(const maple_dirset* ds, int8_t* host_rows) {
+    if (!ds || (!host_rows && ds->size > 0)) return MAPLE_ERR_BAD_ARG;
+    if (ds->size == 0) return MAPLE_OK;
+    maple_ctx* ctx = ds->ctx;
+    CU(cudaMemcpyAsync(host_rows, ds->rows, (size_t)ds->size * ds->n_pad, cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     return MAPLE_OK;
 }
@@ -1261,7 +1272,7 @@ int maple_feasible_starts(maple_ctx* ctx, const int32_t* b, int32_t k, int32_t s
     CU(cudaMemcpyAsync(ctx->fb.p, b, (size_t)m * 4, cudaMemcpyHostToDevice, s));
     CU(ctx->frows.ensure((size_t)k * np));
     if (X_debug) CU(ctx->fX.ensure((size_t)k * n * 4));
-    rc = prepare_set(ctx, std::max<int64_t>(ctx->cand_cap, k), std::max<int64_t>(ctx->pool_cap, k));
+    rc = prepare_set(ctx, std::max<int64_t>(ctx->cand_cap, k), std::max<int64_t>(ctx->pool_cap, k), 0);
     if (rc) return rc;
     FeasibleParams p{};
     p.n = n;

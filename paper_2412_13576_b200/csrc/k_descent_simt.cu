@@ -1,7 +1,7 @@
 // SIMT descent + harvest for general shapes: one warp per start, B in sparse form (the general-shape path;
 // the tcgen05 kernel in k_descent_tc.cu is the fast path for the shapes whose state fits on chip).
 //
-// LLL-reduced kernel bases of the configs are sparse (C2a 4 %, C3 7.6 % nonzeros), so the two
+// LLL-reduced kernel bases of the configs are sparse (C2a 4 %, C3 1.5 %, C5 0.3 % nonzeros), so the two
 // contractions of a step are sparse matrix-vector products, not dense GEMMs:
 //   forward  y_i = sum_{j in row i} B_ij z_j      (each lane owns a load-balanced set of rows)
 //   backward Γ_j = sum_{i in col j} B_ij s_i      (each lane owns a load-balanced set of columns,

@@ -421,8 +421,8 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
                     float* hp = &hi[e >> 2].x;
                     float* lp = &lo[e >> 2].x;
                     const float zz = hp[e & 3] + lp[e & 3];                      // exact
-                    const float2 r2 = __half22float2(*reinterpret_cast<const __half2*>(&rwp[e >> 1]));
-                    const float ro = (e & 1) ? r2.y : r2.x;
+                    // round(z) recomputed from z (the f16 harvest operand is exact only below 2048)
+                    const float ro = round_half_away_f(zz);
                     const float dd = zz - ro;                                   // in [-1/2, 1/2], exact
                     const float sd = dd != 0.f ? copysignf(1.f, dd) : 0.f;
                     // λ1 d/dz (z - floor z)(ceil z - z) = ceil z + floor z - 2z = sign(z - r) - 2 (z - r)

@@ -59,7 +59,6 @@ struct DescentParams {
 
 // SIMT descent + harvest (one warp per start). Returns a cudaError_t.
 cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s);
-cudaError_t launch_descent_tc4(const DescentParams& p, cudaStream_t s);   // same shapes as launch_descent_tc
 // tcgen05 descent + harvest (128 starts per CTA, state resident on chip). Returns cudaErrorNotSupported
 // when the shape does not fit the kernel's tile limits.
 cudaError_t launch_descent_tc(const DescentParams& p, cudaStream_t s);

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lattice.h"
@@ -142,15 +143,43 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
         }
     std::vector<double> mu((size_t)d * d, 0.0), rr((size_t)d * d, 0.0), Bs(d, 0.0);
     auto col = [&](int k) { return &b[(size_t)k * n]; };
+    // nonzero rows of every column (kernel bases are sparse: C5 has ~4 nonzeros per column of 1000), so the inner
+    // products of Gram-Schmidt cost O(nnz) instead of O(n); refreshed whenever a column changes
+    std::vector<std::vector<int>> nz(d);
+    auto refresh = [&](int k) {
+        nz[k].clear();
+        const double* c = col(k);
+        for (int r = 0; r < n; ++r)
+            if (c[r] != 0.0) nz[k].push_back(r);
+    };
+    for (int k = 0; k < d; ++k) refresh(k);
+    auto sdot = [&](int a, int c) {   // exact: integer products and partial sums below 2^53
+        const std::vector<int>& s = nz[a].size() <= nz[c].size() ? nz[a] : nz[c];
+        const double *x = col(a), *y = col(c);
+        double acc = 0.0;
+        for (int r : s) acc += x[r] * y[r];
+        return acc;
+    };
+    // row k of the Gram-Schmidt data: r_kj = <b_k, b_j> - sum_{l<j} mu_jl r_kl. The sum runs over the nonzero
+    // r_kl only (skipping exact zeros leaves every partial sum unchanged), so a sparse, nearly orthogonal basis
+    // costs O(nnz) per row instead of O(k^2)
+    std::vector<int> rnz;
+    rnz.reserve(d);
     auto gso_row = [&](int k) {
         double* rk = &rr[(size_t)k * d];
         double* mk = &mu[(size_t)k * d];
+        rnz.clear();
         for (int j = 0; j < k; ++j) {
-            const double s = dot4(col(k), col(j), n) - dot4(&mu[(size_t)j * d], rk, j);
+            const double* mj = &mu[(size_t)j * d];
+            double s = sdot(k, j);
+            for (int l : rnz) s -= mj[l] * rk[l];
             rk[j] = s;
             mk[j] = s / Bs[j];
+            if (s != 0.0) rnz.push_back(j);
         }
-        Bs[k] = dot4(col(k), col(k), n) - dot4(mk, rk, k);
+        double s = sdot(k, k);
+        for (int l : rnz) s -= mk[l] * rk[l];
+        Bs[k] = s;
     };
     gso_row(0);
     if (Bs[0] <= 0) {
@@ -172,7 +201,7 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
                     double* bk = col(k);
                     const double* bj = col(j);
                     double mx = 0;
-                    for (int r = 0; r < n; ++r) {
+                    for (int r : nz[j]) {
                         bk[r] -= q * bj[r];   // exact: |q|, |b| < 2^20 -> |q b| < 2^40
                         mx = std::fmax(mx, std::fabs(bk[r]));
                     }
@@ -182,6 +211,7 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
                     changed = true;
                 }
             }
+            if (changed) refresh(k);
             if (!changed) break;
         }
         if (Bs[k] <= 0) {
@@ -190,6 +220,7 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
         }
         if (Bs[k - 1] > 2.0 * Bs[k] * (1.0 + 1e-12)) {  // Siegel test (Alg. 1 line 5)
             std::swap_ranges(col(k), col(k) + n, col(k - 1));
+            std::swap(nz[k], nz[k - 1]);
             gso_row(k - 1);
             k = (k - 1 > 1) ? k - 1 : 1;
             if (k == 1) gso_row(0);
@@ -298,6 +329,23 @@ int host_lll(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
 
 namespace {
 
+// f(i) for i in [0, count) on up to hardware_concurrency threads (interleaved indices: the triangular loops below
+// have uneven rows); each i is computed by exactly one thread in the same arithmetic order as serially
+template <class F>
+void parallel_for(int count, F f) {
+    const int nt = std::max(1, std::min<int>((int)std::thread::hardware_concurrency(), std::min(32, count / 16)));
+    if (nt <= 1) {
+        for (int i = 0; i < count; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            for (int i = t; i < count; i += nt) f(i);
+        });
+    for (auto& x : th) x.join();
+}
+
 // B+ fast path (|entries| < 2^20, n <= 8192): G = B^T B exactly in int64 from the rows' outer products (the
 // rows of a reduced kernel basis are sparse), fp64 Cholesky G = L L^T, G^{-1} = L^{-T} L^{-1}, then each column
 // of B+ = G^{-1} (row c of B) touches only the row's nonzeros. Returns 1 when out of range (exact path instead).
@@ -330,24 +378,24 @@ int pinv_fast(const std::vector<int64_t>& B, int n, int d, std::vector<double>& 
             Li[j] = ((double)Gi[(size_t)i * d + j] - dot4(Li, Lj, j)) * inv;
         }
     }
-    // X = L^{-1} (lower triangular), stored transposed (Xt[j][i] = X[i][j]) so both loops below read rows
-    std::vector<double> Xt((size_t)d * d, 0.0), col(d);
-    for (int j = 0; j < d; ++j) {   // column j of X: L x = e_j, x_i = 0 for i < j
-        for (int i = 0; i < d; ++i) col[i] = 0.0;
+    // X = L^{-1} (lower triangular), stored transposed (Xt[j][i] = X[i][j]) so both loops below read rows; the
+    // columns of X are independent triangular solves (one per thread at a time)
+    std::vector<double> Xt((size_t)d * d, 0.0);
+    parallel_for(d, [&](int j) {   // column j of X: L x = e_j, x_i = 0 for i < j, written in place into Xt row j
+        double* col = &Xt[(size_t)j * d];
         col[j] = 1.0 / L[(size_t)j * d + j];
         for (int i = j + 1; i < d; ++i) {
             const double* Li = &L[(size_t)i * d];
             col[i] = -dot4(Li + j, &col[j], i - j) / Li[i];
         }
-        for (int i = j; i < d; ++i) Xt[(size_t)j * d + i] = col[i];
-    }
+    });
     // G^{-1} = X^T X: (G^{-1})_{ab} = sum_{i >= max(a,b)} X_ia X_ib = dot of Xt rows a and b from max(a, b)
     std::vector<double> Ginv((size_t)d * d);
+    parallel_for(d, [&](int a) {   // each thread writes only its own rows (lower triangle): no false sharing
+        for (int b = 0; b <= a; ++b) Ginv[(size_t)a * d + b] = dot4(&Xt[(size_t)a * d + a], &Xt[(size_t)b * d + a], d - a);
+    });
     for (int a = 0; a < d; ++a)
-        for (int b = 0; b <= a; ++b) {
-            const double v = dot4(&Xt[(size_t)a * d + a], &Xt[(size_t)b * d + a], d - a);
-            Ginv[(size_t)a * d + b] = Ginv[(size_t)b * d + a] = v;
-        }
+        for (int b = 0; b < a; ++b) Ginv[(size_t)b * d + a] = Ginv[(size_t)a * d + b];
     Bp.assign((size_t)d * n, 0.0);
     for (int c = 0; c < n; ++c)
         for (const auto& e : rows[c]) {

@@ -31,9 +31,9 @@ def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
     world = dist.get_world_size(group)
     dev = local.device
     k = torch.tensor([local.shape[0]], dtype=torch.int64, device=dev)
-    ks = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-    dist.all_gather(ks, k, group=group)
-    counts = [int(t.item()) for t in ks]
+    ks = torch.empty(world, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(ks, k, group=group)
+    counts = ks.cpu().tolist()                     # one device-to-host read for all ranks' counts
     kmax = max(max(counts), 1)
     stride = local.shape[1]
     pad = torch.zeros((kmax, stride), dtype=local.dtype, device=dev)
@@ -56,13 +56,32 @@ def best_across_ranks(x_best: np.ndarray, f_best: float, device, group=None):
     return best[1:].astype(np.int64), float(best[0])
 
 
+def _on_host(group) -> bool:
+    """gloo exchanges host tensors: the device rows are staged through host memory (CPU staging)."""
+    return dist.get_backend(group) == "gloo"
+
+
 def sharded_extract(ctx, n_total: int, steps: int, lr: float, seed: int, group=None):
-    """Product path (GPU): local maple_extract_range -> NCCL all-gather -> maple_dirset_merge."""
+    """Product path (GPU): local maple_extract_range -> all-gather (NCCL on device buffers; gloo through host
+    staging) -> maple_dirset_merge on the device. Returns (merged set, local set)."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     a, b = shard_range(n_total, rank, world)
     local = ctx.extract_range(n_total, a, b, steps, lr, seed)
     stride = local.stride
-    buf = torch.zeros((max(local.size, 1), stride), dtype=torch.int8, device=f"cuda:{ctx.device}")
+    if _on_host(group):
+        host = torch.from_numpy(np.ascontiguousarray(local.rows_pinned()))          # (k, n) int8
+        if host.shape[1] < stride:
+            host = torch.nn.functional.pad(host, (0, stride - host.shape[1]))
+        rows = gather_rows(host, group)
+        if rows.shape[0] == 0:
+            return ctx.dirset_from_host(np.zeros((0, ctx.n), np.int32)), local
+        dev = rows.to(f"cuda:{ctx.device}")
+        torch.cuda.current_stream().synchronize()
+        return ctx.merge_device(dev.data_ptr(), dev.shape[0], stride), local
+    buf = torch.empty((max(local.size, 1), stride), dtype=torch.int8, device=f"cuda:{ctx.device}")
+    # the allocation is ordered on torch's current stream and the library copies on its own stream: drain the
+    # current stream first (the copy itself is synchronous), so no earlier use of the block can land afterwards
+    torch.cuda.current_stream().synchronize()
     if local.size:
         local.copy_device(buf.data_ptr())
     rows = gather_rows(buf[: local.size], group)
@@ -80,4 +99,4 @@ def sharded_augment(ctx, ds, Q, c, c0, b, X0, group=None, kind=0):
         xb, fb, _, _ = ctx.augment(ds, Q, c, c0, b, X0[a:e], kind=kind)
     else:
         xb, fb = np.zeros(ctx.n, np.int64), float("inf")
-    return best_across_ranks(np.asarray(xb), fb, f"cuda:{ctx.device}", group)
+    return best_across_ranks(np.asarray(xb), fb, "cpu" if _on_host(group) else f"cuda:{ctx.device}", group)

@@ -51,6 +51,7 @@ _SIGS = [
     ("maple_dirset_device_rows", _P, [_P]),
     ("maple_dirset_stride", C.c_int32, [_P]),
     ("maple_dirset_copy_i8", C.c_int, [_P, _P]),
+    ("maple_dirset_copy_raw", C.c_int, [_P, _P]),
     ("maple_dirset_copy_device", C.c_int, [_P, _P]),
     ("maple_dirset_free", None, [_P]),
     ("maple_dirset_from_host", C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(_P)]),
@@ -183,6 +184,19 @@ class DirSet:
         _check(_lib.maple_dirset_copy(self.h, _ptr(out) if out.size else None), self.ctx.h)
         return out
 
+    def rows_pinned(self) -> np.ndarray:
+        """Host rows (size, n) int8 from ONE contiguous DMA into page-locked memory (the stored size x stride rows;
+        a strided view drops the zero padding). The pinned buffer is allocated by torch when it is available."""
+        k, st = self.size, self.stride
+        try:
+            import torch
+            buf = torch.empty((max(k, 1), st), dtype=torch.int8, pin_memory=True).numpy()
+        except Exception:
+            buf = np.empty((max(k, 1), st), dtype=np.int8)
+        if k:
+            _check(_lib.maple_dirset_copy_raw(self.h, _ptr(buf)), self.ctx.h)
+        return buf[:k, :self.ctx.n]
+
     def copy_device(self, dst_ptr: int):
         """Copy the rows (size x stride int8) into device memory at dst_ptr."""
         _check(_lib.maple_dirset_copy_device(self.h, C.c_void_p(dst_ptr)), self.ctx.h)
@@ -248,11 +262,11 @@ class Context:
 
     @property
     def descent_kernel(self) -> str:
-        """'simt', 'tc', 'tc4' or 'tcp' (CTA-pair tcgen05, large shapes): the descent kernel the next extraction
+        """'simt', 'tc' or 'tcp' (CTA-pair tcgen05, large shapes): the descent kernel the next extraction
         launches."""
         r = _lib.maple_descent_kernel(self.h)
         _check(min(r, 0), self.h)
-        return {1: "simt", 2: "tc", 3: "tc4", 4: "tcp"}[r]
+        return {1: "simt", 2: "tc", 4: "tcp"}[r]
 
     def debug_trace(self, enable: bool = True):
         """Arm (enable) or read back the CTA-pair kernel's per-step timeline: (2, 16, 16) uint64 ns stamps."""

@@ -17,7 +17,7 @@ from oracle import postprocess as OP
 pytestmark = pytest.mark.gpu
 
 
-SIMT, TC, TC4 = 1, 2, 3
+SIMT, TC = 1, 2
 
 
 def _ctx(maple, inst, kernel=0):
@@ -53,7 +53,7 @@ def test_basis_and_starts_match_oracle(gpu_lib, name):
     np.testing.assert_allclose(Z0, z0, rtol=1e-12, atol=1e-12)     # fp64 on both sides
 
 
-@pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,T", [("C1", 1), ("C1", 5), ("C2a", 1), ("C2a", 5), ("C2b", 5)])
 def test_descent_iterates_small_T_all_starts(gpu_lib, name, T, kernel):
     from synth import config
@@ -66,7 +66,7 @@ def test_descent_iterates_small_T_all_starts(gpu_lib, name, T, kernel):
     assert _pass_frac(Z, Zo) >= 0.999
 
 
-@pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,T", [("C1", 50), ("C1", 200), ("C2a", 50), ("C2a", 200)])
 def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
     """pass_frac(GPU vs fp64) >= pass_frac(fp32 oracle vs fp64) - 0.005 (the method is chaotic: even exact
@@ -84,7 +84,7 @@ def test_descent_iterates_gate_g2(gpu_lib, name, T, kernel):
     assert gpu >= ref - 0.005
 
 
-@pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,N,filt", [("C1", 1024, 1), ("C1", 1024, 0), ("C2a", 1024, 1), ("C2a", 1024, 0),
                                          ("C2b", 512, 1)])
 def test_postprocess_bit_exact_on_gpu_candidates(gpu_lib, name, N, filt, kernel):
@@ -105,7 +105,7 @@ def test_postprocess_bit_exact_on_gpu_candidates(gpu_lib, name, N, filt, kernel)
     assert ds.pool_size == len(OP.dedupe(cand))
 
 
-@pytest.mark.parametrize("kernel", [SIMT, TC, TC4])
+@pytest.mark.parametrize("kernel", [SIMT, TC])
 @pytest.mark.parametrize("name,N", [("C1", 1024), ("C2a", 1024)])
 def test_sets_match_oracle_g3(gpu_lib, name, N, kernel):
     from synth import config
@@ -241,22 +241,6 @@ def test_tc_and_simt_kernels_agree(gpu_lib, name):
     assert _pass_frac(Zb, Za.astype(np.float64)) >= 0.999
     sa, sb = _set(a.extract(2048, inst.steps, inst.lr, 3).rows()), _set(b.extract(2048, inst.steps, inst.lr, 3).rows())
     assert _jaccard(sa, sb) >= 0.99
-
-
-@pytest.mark.parametrize("name", ["C1", "C2a", "C2b"])
-def test_tc_two_and_four_threads_per_start_bit_identical(gpu_lib, name):
-    """The 2- and 4-thread tcgen05 kernels run the same MMAs and the same per-coordinate arithmetic: identical
-    iterates (bit for bit) and identical extracted sets, including a ragged last CTA."""
-    from synth import config
-    inst = config(name)
-    a, b = _ctx(gpu_lib, inst, TC), _ctx(gpu_lib, inst, TC4)
-    Za, Z0a = a.debug_descent(1000, 0, 1000, 37, inst.lr, 5)
-    Zb, Z0b = b.debug_descent(1000, 0, 1000, 37, inst.lr, 5)
-    np.testing.assert_array_equal(Z0a, Z0b)
-    np.testing.assert_array_equal(Za, Zb)
-    ra = a.extract(3000, inst.steps, inst.lr, 5).rows()
-    rb = b.extract(3000, inst.steps, inst.lr, 5).rows()
-    np.testing.assert_array_equal(ra, rb)
 
 
 @pytest.mark.parametrize("name,N", [("C1", 1024), ("C2a", 8192), ("C2b", 8192), ("C3", 4096)])

@@ -33,7 +33,7 @@ def test_c2a_full_bench_configuration(gpu_lib):
     from synth import c2a
     inst = c2a()
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
-    assert ctx.descent_kernel in ("tc", "tc4")
+    assert ctx.descent_kernel == "tc"
     ds = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
     rows = ds.rows()
     S = _set(rows)
@@ -105,13 +105,18 @@ def _pf(A, R):
 
 
 def _g2(ctx, inst, N, T, seed):
-    """Gate G2: (pass(GPU vs fp64), pass(fp32 oracle vs fp64)) on starts [0, N) after T steps,
-    the oracle's own pseudoinverse of the library's exported basis."""
+    """Gate G2: (pass(GPU vs fp64), pass(fp32 oracle vs fp64), slack) on starts [0, N) after T
+    steps, the oracle's own pseudoinverse of the library's exported basis. The slack is 0.005 or, when larger, two
+    standard errors of the paired difference: in the chaotic regime two equally accurate fp32 evaluations (different
+    summation orders of B z) split on a few percent of the starts at random, sqrt(#discordant) / N."""
     Z, _ = ctx.debug_descent(N, 0, N, T, inst.lr, seed)
     _, z0 = OX.sample_starts(inst.l, inst.u, OL.pinv(ctx.B), seed, np.arange(N))
     Z64 = OX.descend(z0, ctx.B, T, inst.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, T, inst.lr, dtype=np.float32)
-    return _pf(Z, Z64), _pf(Z32, Z64)
+    ok_g = np.all(np.abs(Z.astype(np.float64) - Z64) / np.maximum(1, np.abs(Z64)) <= 1e-4, axis=1)
+    ok_f = np.all(np.abs(Z32.astype(np.float64) - Z64) / np.maximum(1, np.abs(Z64)) <= 1e-4, axis=1)
+    slack = max(0.005, 2.0 * np.sqrt(np.sum(ok_g != ok_f)) / N)
+    return float(ok_g.mean()), float(ok_f.mean()), slack
 
 
 def _g3(ctx, inst, N, rows):
@@ -154,15 +159,15 @@ def test_large_configs_small_sizes(gpu_lib, name, kernel, N, T):
 
 @pytest.mark.parametrize("kernel", [4, 1])
 def test_c3_gates_at_bench_T(gpu_lib, kernel):
-    """C3 at the bench's T (200) and lr: G2 on 512 starts and G3 on 256 starts, both fp32-relative with slack 0.005,
+    """C3 at the bench's T (200) and lr: G2 on 1024 starts (paired slack, see _g2) and G3 on 256 starts (slack 0.005),
     for the CTA-pair tcgen05 kernel (the default) and the SIMT kernel."""
     from synth import c3
     inst = c3()
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
     ctx.set_descent_kernel(kernel)
-    gpu, ref = _g2(ctx, inst, 512, inst.steps, inst.seed)
-    print(f"C3 G2 kernel {kernel}: gpu {gpu:.4f} fp32 {ref:.4f}")
-    assert gpu >= ref - 0.005
+    gpu, ref, slack = _g2(ctx, inst, 1024, inst.steps, inst.seed)
+    print(f"C3 G2 kernel {kernel}: gpu {gpu:.4f} fp32 {ref:.4f} slack {slack:.4f}")
+    assert gpu >= ref - slack
     rows = ctx.extract(256, inst.steps, inst.lr, inst.seed).rows()
     assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
     jg, j32 = _g3(ctx, inst, 256, rows)
@@ -171,16 +176,17 @@ def test_c3_gates_at_bench_T(gpu_lib, kernel):
 
 
 def test_c5_gates_at_bench_T(gpu_lib):
-    """configs[4] (C5: n=1000, m=100, d=900) at T = 200 on 128 starts: G2 and G3, fp32-relative with slack 0.005."""
+    """configs[4] (C5: n=1000, m=100, d=900) at T = 200: G2 on 128 starts and G3 on 2048, fp32-relative (see _g2)."""
     from synth import c5
     inst = c5()
     ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
-    gpu, ref = _g2(ctx, inst, 128, inst.steps, inst.seed)
-    print(f"C5 G2: gpu {gpu:.4f} fp32 {ref:.4f}")
-    assert gpu >= ref - 0.005
-    rows = ctx.extract(128, inst.steps, inst.lr, inst.seed).rows()
+    gpu, ref, slack = _g2(ctx, inst, 128, inst.steps, inst.seed)
+    print(f"C5 G2: gpu {gpu:.4f} fp32 {ref:.4f} slack {slack:.4f}")
+    assert gpu >= ref - slack
+    # C5's binary-box kernel elements are rare (~1 per 70 starts at T = 200): the set gate runs on 2048 starts
+    rows = ctx.extract(2048, inst.steps, inst.lr, inst.seed).rows()
     assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
-    jg, j32 = _g3(ctx, inst, 128, rows)
+    jg, j32 = _g3(ctx, inst, 2048, rows)
     print(f"C5 G3: gpu {jg:.4f} fp32 {j32:.4f}")
     assert jg >= j32 - 0.005
 
@@ -230,8 +236,8 @@ def test_c3_full_size_bench_configuration(gpu_lib):
     """BASELINE configs[2] at its full size on one GPU (2^20 starts, T = 200, the bench's launch): every output
     row is exact (A g = 0, g in the box, g != 0), canonical and lexicographically sorted; sampled rows are
     ⊑-minimal against the WHOLE output set (support-mask prefilter, then the exact test on the host); sampled
-    starts [0, 512) of the same launch configuration pass gate G2 and the sets of starts [0, 256) gate G3 (both
-    fp32-relative, slack 0.005)."""
+    starts [0, 1024) of the same launch configuration pass gate G2 and the sets of starts [0, 256) gate G3 (both
+    fp32-relative)."""
     from synth import c3
     inst = c3()
     assert inst.n_starts == 1 << 20
@@ -257,8 +263,8 @@ def test_c3_full_size_bench_configuration(gpu_lib):
         same = np.all(np.sign(H) * sg >= 0, axis=1) | np.all(np.sign(H) * sg <= 0, axis=1)
         assert int(np.sum(le & same)) == 1                                       # only g itself
     # sampled starts of the same launch: iterates (G2) and sets (G3)
-    gpu, ref = _g2(ctx, inst, 512, inst.steps, inst.seed)
-    assert gpu >= ref - 0.005
+    gpu, ref, slack = _g2(ctx, inst, 1024, inst.steps, inst.seed)
+    assert gpu >= ref - slack
     part = ctx.extract_range(inst.n_starts, 0, 256, inst.steps, inst.lr, inst.seed).rows()
     jg, j32 = _g3(ctx, inst, 256, part)
     assert jg >= j32 - 0.005

@@ -1,0 +1,98 @@
+"""The multi-GPU product path (paper_2412_13576_b200/distributed.py) executed for real on the one
+GPU available: sharded_extract / sharded_augment with NCCL at world size 1, and with gloo at world size 2 (two
+processes, each driving the same GPU with its own context; the exchange goes through host staging, so no kernel
+ever waits on another process). Both must reproduce maple_extract / maple_augment bit for bit: starts are keyed
+by their global index, a locally non-minimal row is globally non-minimal, and the merge re-runs the exact global
+dedupe + ⊑ filter + lexicographic sort."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _reference(name, N, T):
+    from paper_2412_13576_b200 import maple
+    from synth import config
+    maple.load()
+    inst = config(name)
+    ctx = maple.Context(inst.A, inst.l, inst.u)
+    ds = ctx.extract(N, T, inst.lr, inst.seed)
+    from synth import feasible_points
+    X0 = feasible_points(inst, 8, seed=3)
+    xb, fb, _, _ = ctx.augment(ds, inst.Q, inst.c, inst.c0, inst.b, X0)
+    return ds.rows(), np.asarray(xb), fb, X0
+
+
+@pytest.mark.parametrize("name,N,T", [("C2a", 4096, 200), ("C3", 2048, 60)])
+def test_sharded_path_nccl_world1(gpu_lib, name, N, T):
+    from paper_2412_13576_b200 import distributed as D
+    from synth import config
+    ref_rows, ref_x, ref_f, X0 = _reference(name, N, T)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+    try:
+        inst = config(name)
+        ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+        stream = torch.cuda.Stream()
+        ctx.set_stream(stream.cuda_stream)       # the library on its own non-blocking stream, as bench.py runs it
+        merged, local = D.sharded_extract(ctx, N, T, inst.lr, inst.seed)
+        np.testing.assert_array_equal(merged.rows(), ref_rows)
+        np.testing.assert_array_equal(local.rows(), ref_rows)
+        xb, fb = D.sharded_augment(ctx, merged, inst.Q, inst.c, inst.c0, inst.b, X0)
+        assert xb.tolist() == ref_x.tolist() and fb == ref_f
+    finally:
+        dist.destroy_process_group()
+
+
+def _gloo_worker(rank, world, port, name, N, T, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2412_13576_b200 import distributed as D
+        from paper_2412_13576_b200 import maple
+        from synth import config, feasible_points
+        maple.load()
+        inst = config(name)
+        ctx = maple.Context(inst.A, inst.l, inst.u)
+        merged, local = D.sharded_extract(ctx, N, T, inst.lr, inst.seed)
+        X0 = feasible_points(inst, 8, seed=3)
+        xb, fb = D.sharded_augment(ctx, merged, inst.Q, inst.c, inst.c0, inst.b, X0)
+        q.put((rank, merged.rows(), local.size, xb.tolist(), fb))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name,N,T", [("C2a", 4096, 200), ("C3", 2048, 60)])
+def test_sharded_path_gloo_world2(gpu_lib, name, N, T):
+    ref_rows, ref_x, ref_f, _ = _reference(name, N, T)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, name, N, T, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=500) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, rows, local_size, xb, fb in res:
+        np.testing.assert_array_equal(rows, ref_rows)          # every rank ends with the identical global set
+        assert xb == ref_x.tolist() and fb == ref_f
+    assert sum(r[2] for r in res) >= len(ref_rows)            # local sets cover the global one

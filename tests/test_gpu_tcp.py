@@ -69,16 +69,19 @@ def test_tcp_matches_simt_short(gpu_lib, c3):
 
 @pytest.mark.parametrize("T", [50, 200])
 def test_tcp_iterates_gate_g2(gpu_lib, c3, T):
-    """pass(GPU vs fp64) >= pass(fp32 oracle vs fp64) - 0.005 on 256 starts."""
+    """pass(GPU vs fp64) >= pass(fp32 oracle vs fp64) - slack on 1024 starts, slack = max(0.005, two standard errors
+    of the paired difference) (tests/test_gpu_fullsize.py:_g2)."""
     ctx = _ctx(gpu_lib, c3, TCP)
-    N = 256
+    N = 1024
     Z, _ = ctx.debug_descent(N, 0, N, T, c3.lr, c3.seed)
     _, z0 = OX.sample_starts(c3.l, c3.u, OL.pinv(ctx.B), c3.seed, np.arange(N))
     Z64 = OX.descend(z0, ctx.B, T, c3.lr)
     Z32 = OX.descend(z0.astype(np.float32), ctx.B, T, c3.lr, dtype=np.float32)
-    gpu, ref = _pass_frac(Z, Z64), _pass_frac(Z32, Z64)
-    print(f"C3 T={T} tcp: gpu pass {gpu:.4f}, fp32-oracle pass {ref:.4f}")
-    assert gpu >= ref - 0.005
+    ok_g = np.all(np.abs(Z.astype(np.float64) - Z64) / np.maximum(1, np.abs(Z64)) <= 1e-4, axis=1)
+    ok_f = np.all(np.abs(Z32.astype(np.float64) - Z64) / np.maximum(1, np.abs(Z64)) <= 1e-4, axis=1)
+    slack = max(0.005, 2.0 * np.sqrt(np.sum(ok_g != ok_f)) / N)
+    print(f"C3 T={T} tcp: gpu pass {ok_g.mean():.4f}, fp32-oracle pass {ok_f.mean():.4f}, slack {slack:.4f}")
+    assert ok_g.mean() >= ok_f.mean() - slack
 
 
 def test_tcp_postprocess_bit_exact_g1(gpu_lib, c3):
