@@ -89,6 +89,8 @@ class ClockSampler:
         self._p = None
 
     def __enter__(self):
+        if os.environ.get("BENCH_NO_CLOCKS"):   # diagnostics only: the JSON line then reports no clocks
+            return self
         try:
             self._p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                         "--format=csv,noheader,nounits", "-lms", "200"],
@@ -257,16 +259,16 @@ def _roofline(inst, ctx, desc_ms, n_starts_rank, peaks, src, ms):
 def _measure(args, ctx, inst, stream, flush, world, local, one_step, sync_all, steps, warmup):
     """Warm-up, then `steps` timed steps (L2 flushed before each; CUDA events on the library's stream)."""
     import torch
-    for _ in range(warmup):
+    out = None
+    for _ in range(warmup):   # the same pattern as the timed loop: the previous step's result is alive meanwhile
         flush.fill_(1)
-        one_step()
+        out = one_step()
     sync_all()
     launches0 = ctx.launches()
     ev_s = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     ev_e = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     phase = {"descent": [], "dedupe": [], "check": [], "filter": [], "sort": [], "extract_total": [],
              "augment_total": []}
-    out = None
     for k in range(steps):
         flush.fill_(k & 0xFF)              # L2 flush between timed steps (outside the timed region)
         sync_all()
@@ -277,6 +279,9 @@ def _measure(args, ctx, inst, stream, flush, world, local, one_step, sync_all, s
         t = ctx.timings()
         for key in phase:
             phase[key].append(t[key])
+        if os.environ.get("BENCH_VERBOSE"):
+            print(f"[bench] step {k}: {ev_s[k].elapsed_time(ev_e[k]):.2f} ms " +
+                  " ".join(f"{key} {t[key]:.2f}" for key in phase), file=sys.stderr)
     step_ms = [ev_s[k].elapsed_time(ev_e[k]) for k in range(steps)]
     return float(np.mean(step_ms)), phase, ctx.launches() - launches0, out
 

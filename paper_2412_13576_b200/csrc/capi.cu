@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -290,8 +291,12 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
                       counters(ctx) + C_KEEP, counters(ctx) + C_NZMAX, s));
     ctx->launches++;
     CU(cudaEventRecord(ctx->ev[4], s));
+    static const bool htrace = getenv("MAPLE_HOST_TRACE") != nullptr;
+    auto hnow = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    const double th0 = htrace ? hnow() : 0.0;
     unsigned long long h[C_N];
     int rc = read_counters(ctx, h);
+    const double th1 = htrace ? hnow() : 0.0;
     if (rc) return rc;
     if (h[C_RANGE]) {   // the CTA-pair kernel's f16 operands overflowed (|z| > 60000): redo this extraction on SIMT
         ctx->tcp_range_fail = true;
@@ -316,13 +321,21 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
         delete ds;
         CU(e);
     }
+    const double th2 = htrace ? hnow() : 0.0;
     CU(ctx->sortkeys.ensure(std::max<int64_t>(M, 1) * np));
     CU(ctx->sidx0.ensure(std::max<int64_t>(M, 1) * 4));
     CU(ctx->sidx1.ensure(std::max<int64_t>(M, 1) * 4));
+    const double th3 = htrace ? hnow() : 0.0;
     nl = 0;
     CU(launch_lex_sort(ctx->tmp_rows.as<int8_t>(), M, ctx->n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
                        ctx->sidx1.as<int32_t>(), ds->rows, s, &nl));
     ctx->launches += nl;
+    if (htrace) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fprintf(stderr, "[maple host] finish_set: counters %.3f ms, rows alloc %.3f ms, ensure %.3f ms, sort launch %.3f ms "
+                "(M=%lld, free %.1f GB)\n", th1 - th0, th2 - th1, th3 - th2, hnow() - th3, (long long)M, fr / 1e9);
+    }
     CU(cudaEventRecord(ctx->ev[5], s));
     if (cudaEventCreateWithFlags(&ds->ready, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(ds->ready, s);
     ctx->timings_pending = true;
