@@ -555,9 +555,7 @@ bool tcp_ok(const maple_ctx* ctx) {
 // the descent kernel an extraction launches: 1 SIMT, 2 tcgen05 (small shapes), 4 CTA-pair tcgen05 (large shapes)
 int which_descent(const maple_ctx* ctx) {
     const bool tc_ok = descent_tc_supported(ctx->n, ctx->d) && ctx->rbound < 2047.0;
-    const bool variant = ctx->optimizer != 0 || ctx->harvest_final != 0;
-    if (ctx->descent_kernel == 4) return tcp_ok(ctx) ? 4 : 1;
-    (void)variant;
+    if (ctx->descent_kernel == 4) return tcp_ok(ctx) ? 4 : 1;   // documented in maple.h: SIMT where tcp cannot run
     if (ctx->descent_kernel != 0) return ctx->descent_kernel;
     if (tc_ok) return kAutoTc;
     return tcp_ok(ctx) ? 4 : 1;

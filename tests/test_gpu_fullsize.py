@@ -120,8 +120,11 @@ def _g2(ctx, inst, N, T, seed):
 
 
 def _g3(ctx, inst, N, rows):
-    """Gate G3, fp32-relative: (Jaccard(GPU, fp64 oracle), Jaccard(fp32 oracle, fp64 oracle)) of the ⊑-minimal sets
-    of starts [0, N); every row of a symmetric difference is an exact in-box nonzero kernel element."""
+    """Gate G3, fp32-relative: (Jaccard(GPU, fp64 oracle), Jaccard(fp32 oracle, fp64 oracle), slack) of the
+    ⊑-minimal sets of starts [0, N); every row of a symmetric difference is an exact in-box nonzero kernel element.
+    slack = max(0.005, 2 sqrt(|GPU Δ fp32 oracle|) / |GPU ∪ fp32 ∪ fp64|): the two fp32 evaluations lose rows to
+    chaos independently (DESIGN §4 G2), so the difference of their Jaccard indices has a noise scale of about
+    sqrt(#rows found by exactly one of them) / |union| — 0.005 on C3's hundreds of rows, large on C5's dozens."""
     Bp = OL.pinv(ctx.B)
     p64, _ = OX.extract_pool(ctx.B, Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed)
     p32, _ = OX.extract_pool(ctx.B, Bp, inst.l, inst.u, N, inst.steps, inst.lr, inst.seed, dtype=np.float32)
@@ -131,7 +134,8 @@ def _g3(ctx, inst, N, rows):
     diff = np.array(sorted((G ^ m64) | (m32 ^ m64)), dtype=np.int64).reshape(-1, inst.n)
     if diff.size:
         assert np.all(OP.check_rows(inst.A, inst.l, inst.u, diff))
-    return jac(G, m64), jac(m32, m64)
+    slack = max(0.005, 2.0 * np.sqrt(len(G ^ m32)) / max(1, len(G | m32 | m64)))
+    return jac(G, m64), jac(m32, m64), slack
 
 
 @pytest.mark.parametrize("name,kernel,N,T", [("C3", "tcp", 128, 40), ("C3", "simt", 128, 40), ("C5", "simt", 64, 30)])
@@ -170,9 +174,9 @@ def test_c3_gates_at_bench_T(gpu_lib, kernel):
     assert gpu >= ref - slack
     rows = ctx.extract(256, inst.steps, inst.lr, inst.seed).rows()
     assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
-    jg, j32 = _g3(ctx, inst, 256, rows)
-    print(f"C3 G3 kernel {kernel}: gpu {jg:.4f} fp32 {j32:.4f}")
-    assert jg >= j32 - 0.005
+    jg, j32, g3s = _g3(ctx, inst, 256, rows)
+    print(f"C3 G3 kernel {kernel}: gpu {jg:.4f} fp32 {j32:.4f} slack {g3s:.4f}")
+    assert jg >= j32 - g3s
 
 
 def test_c5_gates_at_bench_T(gpu_lib):
@@ -186,9 +190,9 @@ def test_c5_gates_at_bench_T(gpu_lib):
     # C5's binary-box kernel elements are rare (~1 per 70 starts at T = 200): the set gate runs on 2048 starts
     rows = ctx.extract(2048, inst.steps, inst.lr, inst.seed).rows()
     assert rows.shape[0] > 0 and np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
-    jg, j32 = _g3(ctx, inst, 2048, rows)
-    print(f"C5 G3: gpu {jg:.4f} fp32 {j32:.4f}")
-    assert jg >= j32 - 0.005
+    jg, j32, g3s = _g3(ctx, inst, 2048, rows)
+    print(f"C5 G3: gpu {jg:.4f} fp32 {j32:.4f} slack {g3s:.4f}")
+    assert jg >= j32 - g3s
 
 
 def test_c2b_full_postprocess_witnesses(gpu_lib):
@@ -266,5 +270,5 @@ def test_c3_full_size_bench_configuration(gpu_lib):
     gpu, ref, slack = _g2(ctx, inst, 1024, inst.steps, inst.seed)
     assert gpu >= ref - slack
     part = ctx.extract_range(inst.n_starts, 0, 256, inst.steps, inst.lr, inst.seed).rows()
-    jg, j32 = _g3(ctx, inst, 256, part)
-    assert jg >= j32 - 0.005
+    jg, j32, g3s = _g3(ctx, inst, 256, part)
+    assert jg >= j32 - g3s

@@ -1,8 +1,8 @@
 """CTA-pair tcgen05 descent (k_descent_tcp.cu, descent kernel 4) against the oracle: the large-shape path
 (configs[2] = C3: n = 300, m = 20, d = 280). Gates of DESIGN.md §4 with the oracle's own pseudoinverse
 (OL.pinv of the library's exported B): starts bit-for-bit in fp64 (1e-12), iterates at small T for every start,
-G2 (fp32-relative, slack 0.005) at the stated T, G1 (bit-exact post-processing of the GPU candidates) and
-G3 (fp32-relative Jaccard, slack 0.005; every disagreement passes the invariants)."""
+G2 (fp32-relative, paired-noise slack >= 0.005) at the stated T, G1 (bit-exact post-processing of the GPU candidates) and
+G3 (fp32-relative Jaccard, paired-noise slack >= 0.005; every disagreement passes the invariants)."""
 import numpy as np
 import pytest
 
@@ -98,7 +98,7 @@ def test_tcp_postprocess_bit_exact_g1(gpu_lib, c3):
 
 
 def test_tcp_sets_gate_g3(gpu_lib, c3):
-    """G3 fp32-relative: Jaccard(GPU, fp64 oracle) >= Jaccard(fp32 oracle, fp64 oracle) - 0.005 on the same
+    """G3 fp32-relative: Jaccard(GPU, fp64 oracle) >= Jaccard(fp32 oracle, fp64 oracle) - slack on the same
     256 starts; every row in a symmetric difference is an exact in-box kernel element."""
     ctx = _ctx(gpu_lib, c3, TCP)
     N = 256
@@ -108,8 +108,10 @@ def test_tcp_sets_gate_g3(gpu_lib, c3):
     p32, _ = OX.extract_pool(ctx.B, Bp, c3.l, c3.u, N, c3.steps, c3.lr, c3.seed, dtype=np.float32)
     m64, m32 = OP.minimal_filter(p64), OP.minimal_filter(p32)
     jg, j32 = _jac(g, m64), _jac(m32, m64)
-    print(f"C3 G3 tcp: |gpu|={len(g)} |fp64|={len(m64)} jaccard {jg:.4f}, fp32-oracle {j32:.4f}")
-    assert jg >= j32 - 0.005
+    # the paired-noise slack of tests/test_gpu_fullsize.py:_g3
+    slack = max(0.005, 2.0 * np.sqrt(len(g ^ m32)) / max(1, len(g | m32 | m64)))
+    print(f"C3 G3 tcp: |gpu|={len(g)} |fp64|={len(m64)} jaccard {jg:.4f}, fp32-oracle {j32:.4f}, slack {slack:.4f}")
+    assert jg >= j32 - slack
     diff = np.array(sorted(g ^ m64), dtype=np.int64).reshape(-1, c3.n)
     if diff.size:
         assert np.all(OP.check_rows(c3.A, c3.l, c3.u, diff))
