@@ -233,8 +233,11 @@ int maple_descent_kernel(const maple_ctx* ctx);
  * whose kernel would be 4 runs SIMT. Returns BAD_ARG for a null context or out-of-range values. Host only. */
 int maple_set_descent_variant(maple_ctx* ctx, int32_t optimizer, int32_t harvest_final);
 /* Select the ⊑-minimality filter's pair enumeration (Def. 1-2; the kept set is the same for all):
- * 0 = auto (indexed when n <= 1024), 1 = tiled (every row against all rows of smaller L1 norm), 2 = indexed
- * (every row against the rows filed under one of its support coordinates with smaller L1 norm; needs n <= 1024).
+ * 0 = auto (level-synchronous when n <= 1024, else tiled), 1 = tiled (every row against all rows of smaller L1
+ * norm), 2 = indexed (every row against the rows filed under one of its support coordinates with smaller L1 norm),
+ * 3 = level-synchronous (L1 levels in increasing order, every row against the ⊑-minimal rows of smaller L1 filed
+ * under its support coordinates — sufficient because ⊑ is a partial order — tested 32 rows at a time with
+ * bit-sliced fold masks; one cooperative launch). 2 and 3 need n <= 1024 (else tiled).
  * Returns BAD_ARG for a null context or another value. Host only. */
 int maple_set_filter_algorithm(maple_ctx* ctx, int32_t which);
 

@@ -118,11 +118,12 @@ struct maple_ctx {
     bool tcp_range_fail = false;  // an extraction saw an iterate beyond the f16 operand range: use SIMT from now on
     DevBuf trace;                 // debug timeline of the CTA-pair kernel (maple_debug_trace)
     bool trace_on = false;
-    int filter_algo = 0;          // 0 auto (indexed), 1 tiled, 2 indexed
+    int filter_algo = 0;          // 0 auto (kAutoFilter), 1 tiled, 2 indexed, 3 level-synchronous
     int optimizer = 0;            // reading #24: 0 Adam, 1 GD, 2 sign-GD
     int harvest_final = 0;        // reading #25: 1 = harvest the final iterate only
     // workspace
     DevBuf ffreq, fkey, fbh, fbs, fbc, flrow, flsig;   // indexed filter (k_post.cu)
+    DevBuf fgc, fgs, fgr, fhf;                         // level-synchronous filter: G lists, list fill counters
     DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, sig, l1, hist, level_start, cursor, order, keep,
         witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
     DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b, atab, atoff;
@@ -203,6 +204,15 @@ int read_counters(maple_ctx* ctx, unsigned long long* h) {
     return MAPLE_OK;
 }
 
+constexpr int kAutoFilter = 3;   // auto choice of the ⊑ filter's pair enumeration (n <= 1024)
+
+// the ⊑ filter's pair enumeration: 1 tiled, 2 tiled prefix + key-coordinate index, 3 tiled prefix + level-synchronous
+// minimal-row index (n <= 1024 for 2 and 3)
+int resolved_filter_algo(const maple_ctx* ctx) {
+    if (ctx->filter_algo == 1 || ctx->n > 1024) return 1;
+    return ctx->filter_algo == 0 ? kAutoFilter : ctx->filter_algo;
+}
+
 // Size the candidate buffer, the hash set (pool + table) and the per-row work buffers, then reset the set.
 int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap, int filter_minimal) {
     const int np = ctx->n_pad;
@@ -247,6 +257,12 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap, int filter_m
         CU(ctx->fbh.ensure(nbins * 4));
         CU(ctx->fbs.ensure((nbins + 1) * 4));
         CU(ctx->fbc.ensure(nbins * 4 + 4));   // + the undecided-row counter
+        if (filter_minimal && resolved_filter_algo(ctx) == 3) {
+            CU(ctx->fgc.ensure(nbins * 4));
+            CU(ctx->fgs.ensure((nbins + 1) * 4));
+            CU(ctx->fgr.ensure((size_t)ctx->pool_cap * ctx->n * 4));
+            CU(ctx->fhf.ensure((size_t)ctx->n * 4 + 8));   // + the level kernel's grid barrier words
+        }
     }
     CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));
     CU(cudaMemsetAsync(ctx->idx.p, 0xFF, (size_t)ctx->pool_cap * 8, ctx->stream));
@@ -275,10 +291,11 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
                   ctx->th_c1.as<int32_t>(), ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
                   ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh, ctx->sig.as<uint4>(),
-                  ctx->filter_algo == 1 || ctx->n > 1024 ? 1 : 2, 0, ctx->pool.as<int8_t>(), ctx->ffreq.as<int32_t>(),
+                  resolved_filter_algo(ctx), 0, ctx->pool.as<int8_t>(), ctx->ffreq.as<int32_t>(),
                   ctx->fkey.as<int32_t>(), ctx->fbh.as<int32_t>(), ctx->fbs.as<int32_t>(), ctx->fbc.as<int32_t>(),
                   ctx->flrow.as<int32_t>(), ctx->flsig.as<uint4>(),
-                  ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1)};
+                  ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1), ctx->fgc.as<int32_t>(),
+                  ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>()};
     const unsigned long long* dpool = counters(ctx) + C_POOL;
     CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, filter_minimal, ctx->flags.as<uint8_t>(),
                           counters(ctx) + C_BAD, s));
@@ -860,7 +877,7 @@ int maple_set_descent_variant(maple_ctx* ctx, int32_t optimizer, int32_t harvest
 }
 
 int maple_set_filter_algorithm(maple_ctx* ctx, int32_t which) {
-    if (!ctx || which < 0 || which > 2) return MAPLE_ERR_BAD_ARG;
+    if (!ctx || which < 0 || which > 3) return MAPLE_ERR_BAD_ARG;
     ctx->filter_algo = which;
     return MAPLE_OK;
 }

@@ -583,6 +583,282 @@ __global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork f
     }
 }
 
+// ---- level-synchronous filter over ⊑-minimal rows (algo 3) ----
+// If some row h ⊑ ±g, then some ⊑-minimal row m ⊑ h ⊑ ±g (⊑ is a partial order on the finite pool), and
+// L1(m) < L1(g). So g is dominated iff a MINIMAL row of smaller L1 dominates it, and g need only meet those.
+// Levels L = 1, 2, ... (L1 norms) are decided in order: the rows of level L that the tiled prefix left undecided
+// are tested against the minimal rows of levels < L filed under their support coordinates (key coordinate
+// κ(h) ∈ supp(h) ⊆ supp(g), as in the indexed filter); then level L's minimal rows are appended to their key
+// coordinate's list. The pairs are blocked coordinate-major: a work item is (c, 256 rows g of level L with
+// c ∈ supp(g), a segment of c's list), the list tiles staged in shared memory and shared by the 256 rows.
+// The keep bit is defined pairwise, so it equals the other algorithms' (only the witness may differ).
+constexpr int kLvThreads = 256, kLvTile = 512, kLvSeg = 4096;
+
+// G lists: every undecided row g (keep == 2) is filed under bin L1(g) n + c for each c ∈ supp(g);
+// pass 0 counts (gl_cursor as histogram), pass 1 scatters (gl_cursor as cursor)
+__global__ void glist_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap, int pass) {
+    if (*fw.n_undec == 0) return;
+    const int64_t count = dev_count(dcount, cap);
+    const int nw = fw.n_pad / 16, n = fw.n;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
+        if (fw.keep[r] != 2) continue;
+        const int base = fw.l1[r] * n;
+        const int4* g = reinterpret_cast<const int4*>(fw.rows + (size_t)r * fw.n_pad);
+        for (int w = 0; w < nw; ++w) {
+            const int4 v = g[w];
+            const uint32_t q[4] = {(uint32_t)v.x, (uint32_t)v.y, (uint32_t)v.z, (uint32_t)v.w};
+#pragma unroll
+            for (int b = 0; b < 16; ++b)
+                if ((q[b >> 2] >> (8 * (b & 3))) & 0xFFu) {
+                    int32_t* slot = &fw.gl_cursor[base + 16 * w + b];
+                    if (pass == 0) atomicAdd(slot, 1);
+                    else fw.gl_rows[atomicAdd(slot, 1)] = (int32_t)r;
+                }
+        }
+    }
+}
+
+// exclusive scan of hist[0, nb) into start[0, nb] and cursor[0, nb): one block of 1024 threads
+__global__ void __launch_bounds__(1024) scan_bins_kernel(const int32_t* n_undec, int32_t* hist, int nb, int32_t* start,
+                                                         int32_t* cursor) {
+    if (*n_undec == 0) return;
+    __shared__ int32_t part[1024];
+    const int t = threadIdx.x;
+    const int chunk = (nb + 1023) / 1024;
+    const int b0 = min(nb, t * chunk), b1 = min(nb, b0 + chunk);
+    int32_t acc = 0;
+    for (int b = b0; b < b1; ++b) acc += hist[b];
+    part[t] = acc;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {
+        const int32_t v = t >= off ? part[t - off] : 0;
+        __syncthreads();
+        part[t] += v;
+        __syncthreads();
+    }
+    int32_t run = part[t] - acc;
+    for (int b = b0; b < b1; ++b) {   // (cursor may alias hist)
+        const int32_t h = hist[b];
+        start[b] = run;
+        cursor[b] = run;
+        run += h;
+    }
+    if (t == 1023) start[nb] = part[1023];
+}
+
+// Bit-sliced pair test. A warp owns 32 rows g (lane j: g_j) and keeps, for every fold bit b, the 32-bit masks
+// {j : b ∈ fold(P_gj)} and {j : b ∈ fold(N_gj)} in shared memory. A lane takes one list row h and intersects the
+// masks of h's fold bits: h ⊑ g_j needs fold(P_h) ⊆ fold(P_gj) and fold(N_h) ⊆ fold(N_gj) (bit j survives the ANDs
+// over P_h's bits of the P masks and over N_h's bits of the N masks), h ⊑ -g_j the same with P and N of g exchanged.
+// So one lane tests h against 32 rows at once and stops as soon as no row survives (usually after a few bits); the
+// surviving (h, g_j) pairs get the exact test on the full codes.
+__device__ void level_tile(const FilterWork& fw, int L) {
+    constexpr int NWARP = kLvThreads / 32;
+    __shared__ int32_t pre[kIdxMaxN + 1];
+    __shared__ uint4 tsig[kLvTile];
+    __shared__ int32_t trow[kLvTile];
+    __shared__ uint2 mk[NWARP][64];        // per warp, fold bit b: (P mask, N mask) over its 32 rows
+    __shared__ int32_t grow[NWARP][32];    // the warp's rows g
+    __shared__ uint32_t dead[NWARP];       // rows of the warp found dominated in this item
+    const int n = fw.n, Wh = fw.Wh, W2 = 2 * Wh, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int32_t* gs = fw.gl_start + (size_t)L * n;
+    const int lb = fw.Lmax + 1;
+    // work items per coordinate: ceil(|G_{L,c}| / 256) x ceil(|H_c| / kLvSeg); block-wide exclusive scan over c
+    {
+        constexpr int PER = (kIdxMaxN + kLvThreads - 1) / kLvThreads;
+        int32_t v[PER], acc = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int c = tid * PER + k;
+            int32_t it = 0;
+            if (c < n) {
+                const int32_t ng = gs[c + 1] - gs[c], nh = fw.h_fill[c];
+                it = ((ng + kLvThreads - 1) / kLvThreads) * ((nh + kLvSeg - 1) / kLvSeg);
+            }
+            v[k] = acc;
+            acc += it;
+        }
+        __shared__ int32_t wsum[NWARP];
+        int32_t x = acc;   // inclusive warp scan of the per-thread totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[wid] = x;
+        __syncthreads();
+        if (tid == 0) {
+            int32_t run = 0;
+            for (int w = 0; w < NWARP; ++w) {
+                const int32_t t2 = wsum[w];
+                wsum[w] = run;
+                run += t2;
+            }
+        }
+        __syncthreads();
+        const int32_t excl = x - acc + wsum[wid];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int c = tid * PER + k;
+            if (c <= n) pre[c] = excl + v[k];
+        }
+        if (tid == kLvThreads - 1 && (tid + 1) * PER <= n) pre[n] = excl + acc;
+        __syncthreads();
+    }
+    const int32_t total = pre[n];
+    volatile uint8_t* vkeep = fw.keep;
+    for (int32_t item = blockIdx.x; item < total; item += gridDim.x) {
+        int lo = 0, hi = n;   // the coordinate c with pre[c] <= item < pre[c + 1]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pre[mid] <= item) lo = mid;
+            else hi = mid;
+        }
+        const int c = lo;
+        const int32_t nh = fw.h_fill[c];
+        const int32_t nseg = (nh + kLvSeg - 1) / kLvSeg;
+        const int32_t local = item - pre[c], gi = local / nseg, si = local % nseg;
+        const int32_t e = gs[c] + gi * kLvThreads + tid;
+        int32_t g = -1;
+        if (e < gs[c + 1]) g = fw.gl_rows[e];
+        const bool mine = g >= 0 && vkeep[g] == 2;
+        uint32_t alive = __ballot_sync(0xffffffffu, mine);
+        const uint4 sg = mine ? fw.sig[g] : make_uint4(0u, 0u, 0u, 0u);
+        grow[wid][lane] = g;
+        if (lane == 0) dead[wid] = 0u;
+        // transpose the 32 rows' folds into per-bit masks: lane b writes bits b and b + 32
+#pragma unroll 4
+        for (int b = 0; b < 32; ++b) {
+            const uint32_t p0 = __ballot_sync(0xffffffffu, (sg.x >> b) & 1u), p1 = __ballot_sync(0xffffffffu, (sg.y >> b) & 1u);
+            const uint32_t n0 = __ballot_sync(0xffffffffu, (sg.z >> b) & 1u), n1 = __ballot_sync(0xffffffffu, (sg.w >> b) & 1u);
+            if (lane == b) {
+                mk[wid][b] = make_uint2(p0, n0);
+                mk[wid][b + 32] = make_uint2(p1, n1);
+            }
+        }
+        __syncwarp();
+        const int32_t h0 = fw.bin_start[c * lb] + si * kLvSeg;
+        const int32_t h1 = min(fw.bin_start[c * lb] + nh, h0 + kLvSeg);
+        for (int32_t t0 = h0; t0 < h1; t0 += kLvTile) {
+            if (!__syncthreads_or(alive != 0u)) break;
+            const int lim = min(kLvTile, h1 - t0);
+            for (int i = tid; i < lim; i += kLvThreads) {
+                tsig[i] = fw.list_sig[t0 + i];
+                trow[i] = fw.list_row[t0 + i];
+            }
+            __syncthreads();
+            // rows another item (or another warp's exact test) has decided meanwhile
+            alive &= __ballot_sync(0xffffffffu, g >= 0 && vkeep[g] == 2) & ~dead[wid];
+            for (int i0 = 0; i0 < lim && alive; i0 += 32) {
+                const int i = i0 + lane;
+                uint32_t pos = 0u, neg = 0u;
+                if (i < lim) {
+                    const uint4 hs = tsig[i];
+                    pos = alive;
+                    neg = alive;
+                    uint64_t fp = ((uint64_t)hs.y << 32) | hs.x, fn = ((uint64_t)hs.w << 32) | hs.z;
+                    while (fp && (pos | neg)) {
+                        const int b = __ffsll((long long)fp) - 1;
+                        fp &= fp - 1;
+                        const uint2 m = mk[wid][b];
+                        pos &= m.x;
+                        neg &= m.y;
+                    }
+                    while (fn && (pos | neg)) {
+                        const int b = __ffsll((long long)fn) - 1;
+                        fn &= fn - 1;
+                        const uint2 m = mk[wid][b];
+                        pos &= m.y;
+                        neg &= m.x;
+                    }
+                }
+                uint32_t cand = pos | neg;
+                if (cand) {   // exact test on the codes for the surviving (h, g_j)
+                    const int32_t hr = trow[i];
+                    const uint32_t* hc = fw.codes + (size_t)hr * W2;
+                    while (cand) {
+                        const int j = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        const int32_t gj = grow[wid][j];
+                        const uint32_t* gc = fw.codes + (size_t)gj * W2;
+                        uint32_t pos_v = 0, neg_v = 0;
+                        for (int w = 0; w < Wh; ++w) {
+                            const uint32_t hp = hc[w], hn = hc[Wh + w], gp = gc[w], gn = gc[Wh + w];
+                            pos_v |= (hp & ~gp) | (hn & ~gn);
+                            neg_v |= (hp & ~gn) | (hn & ~gp);
+                        }
+                        if (pos_v == 0u || neg_v == 0u) {
+                            fw.witness[gj] = hr;
+                            vkeep[gj] = 0;
+                            atomicOr(&dead[wid], 1u << j);
+                        }
+                    }
+                }
+                __syncwarp();
+                alive &= ~dead[wid];
+            }
+        }
+        __syncthreads();   // the tile buffers and masks are reused by the next item
+    }
+}
+
+// level L decided: its remaining undecided rows are minimal; every minimal row of level L joins its key
+// coordinate's list (the lists hold the minimal rows of the levels below the one being tested)
+__device__ void level_append(const FilterWork& fw, int L) {
+    const int32_t lo = fw.level_start[L], hi = fw.level_start[L + 1];
+    const int lb = fw.Lmax + 1;
+    for (int32_t q = lo + blockIdx.x * blockDim.x + threadIdx.x; q < hi; q += gridDim.x * blockDim.x) {
+        const int32_t r = fw.order[q];
+        uint8_t k = fw.keep[r];
+        if (k == 2) {
+            k = 1;
+            fw.keep[r] = 1;
+        }
+        if (k == 1) {
+            const int c = fw.key_bin[r] / lb;
+            const int32_t p = fw.bin_start[c * lb] + atomicAdd(&fw.h_fill[c], 1);
+            fw.list_row[p] = r;
+            fw.list_sig[p] = fw.sig[r];
+        }
+    }
+}
+
+// grid-wide barrier for the co-resident (cooperatively launched) level kernel: arrival count + generation
+__device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = gen;
+        const unsigned g0 = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g0) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// All levels in one cooperative launch: level L's tile phase (if it has undecided rows) runs between two grid
+// barriers — after every lower level's appends, before its own — and appends need no barrier of their own (a
+// coordinate's list order is irrelevant). Returns at once when the tiled prefix decided every row.
+__global__ void __launch_bounds__(kLvThreads) level_filter_kernel(FilterWork fw, unsigned* bar) {
+    if (*fw.n_undec == 0) return;
+    const int n = fw.n;
+    for (int L = 1; L <= fw.Lmax; ++L) {
+        if (fw.level_start[L] == fw.level_start[L + 1]) continue;   // no row has L1 = L
+        if (fw.gl_start[(size_t)(L + 1) * n] > fw.gl_start[(size_t)L * n]) {
+            grid_barrier(bar, bar + 1);
+            level_tile(fw, L);
+            grid_barrier(bar, bar + 1);
+        }
+        level_append(fw, L);
+    }
+}
+
 __global__ void keep_valid_kernel(const uint8_t* valid, const unsigned long long* dcount, int64_t cap, uint8_t* keep,
                                   int32_t* witness) {
     const int64_t count = dev_count(dcount, cap);
@@ -834,9 +1110,38 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
     }
     cudaError_t e;
     const int algo = fw.algo;
-    fw.scan_cap = algo == 2 ? 2 * kTile : 0x7fffffff;
+    fw.scan_cap = algo >= 2 ? 2 * kTile : 0x7fffffff;
     if ((e = cudaMemsetAsync(fw.n_undec, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
     if ((e = launch_filter_tiled(dcount, cap, fw, s, launches)) != cudaSuccess) return e;
+    if (algo == 3) {   // rows the prefix did not decide: level by level against the minimal rows below
+        if (fw.n > kIdxMaxN) return cudaErrorInvalidValue;
+        const int lb = fw.Lmax + 1;
+        const int nbins = fw.n * lb;
+        if ((e = cudaMemsetAsync(fw.freq, 0, sizeof(int32_t) * fw.n, s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(fw.bin_hist, 0, sizeof(int32_t) * nbins, s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(fw.gl_cursor, 0, sizeof(int32_t) * nbins, s)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(fw.h_fill, 0, sizeof(int32_t) * fw.n, s)) != cudaSuccess) return e;
+        coord_freq_kernel<<<grid_for(cap, 256, 148 * 4), 256, 0, s>>>(fw, dcount, cap);
+        key_bin_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(fw, dcount, cap);
+        bin_scan_kernel<<<1, 1024, 0, s>>>(fw, nbins);   // bin_start: each key coordinate's list capacity
+        glist_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(fw, dcount, cap, 0);
+        scan_bins_kernel<<<1, 1024, 0, s>>>(fw.n_undec, fw.gl_cursor, nbins, fw.gl_start, fw.gl_cursor);
+        glist_kernel<<<grid_for(cap, 256, 148 * 8), 256, 0, s>>>(fw, dcount, cap, 1);
+        *launches += 6;
+        int per_sm = 0, dev = 0, nsm = 148;
+        if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, level_filter_kernel, kLvThreads, 0)) != cudaSuccess)
+            return e;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const int grid = std::max(1, per_sm) * nsm;
+        unsigned* bar = reinterpret_cast<unsigned*>(fw.h_fill + fw.n);   // 2 words after the fill counters
+        if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s)) != cudaSuccess) return e;
+        void* args[] = {&fw, &bar};
+        if ((e = cudaLaunchCooperativeKernel((void*)level_filter_kernel, grid, kLvThreads, args, 0, s)) != cudaSuccess)
+            return e;
+        *launches += 1;
+        return cudaGetLastError();
+    }
     if (algo == 2) {   // rows the prefix did not decide: indexed by key coordinate and L1
         if (fw.n > kIdxMaxN) return cudaErrorInvalidValue;
         const int nbins = fw.n * (fw.Lmax + 1);

@@ -116,7 +116,8 @@ struct FilterWork {
     int32_t* witness;             // count
     int Lmax;
     uint4* sig;                   // count: 64-bit folds (bit i mod 64) of the two code halves (the filter's prefilter)
-    int algo;                     // 1: tiled scan of all lower-L1 rows; 2: tiled prefix, then indexed by key coordinate
+    int algo;                     // 1: tiled scan of all lower-L1 rows; 2: tiled prefix, then indexed by key coordinate;
+                                  // 3: tiled prefix, then level-synchronous over minimal rows (coordinate-major tiles)
     int scan_cap;                 // tiled scan: rows of smaller L1 scanned per row (set by launch_filter)
     const int8_t* rows;           // the rows themselves (stride n_pad): supports, for the indexed filter
     int32_t* freq;                // n: rows having coordinate i in their support
@@ -127,6 +128,11 @@ struct FilterWork {
     int32_t* list_row;            // count: rows in bin order
     uint4* list_sig;              // count: their folds, in bin order
     int32_t* n_undec;             // rows the tiled prefix left undecided (the index is built only if > 0)
+    // level-synchronous filter (algo 3)
+    int32_t* gl_cursor;           // (Lmax + 1) n: histogram, then cursor of the G lists (undecided rows by (L1, c))
+    int32_t* gl_start;            // (Lmax + 1) n + 1
+    int32_t* gl_rows;             // sum of |supp| over the undecided rows (capacity count x n)
+    int32_t* h_fill;              // n: minimal rows appended so far to each key coordinate's list
 };
 // flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= u - l (conditions C1-C3), for the first
 // min(*dcount, cap) rows; with encode != 0 also the filter's thermometer codes and L1 norms.

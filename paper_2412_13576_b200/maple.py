@@ -257,7 +257,8 @@ class Context:
         _check(_lib.maple_set_descent_variant(self.h, code, int(harvest_final)), self.h)
 
     def set_filter_algorithm(self, which: int):
-        """0 auto, 1 tiled, 2 indexed (maple_set_filter_algorithm): same kept set, different pair enumeration."""
+        """0 auto, 1 tiled, 2 indexed, 3 level-synchronous (maple_set_filter_algorithm): same kept set, different
+        pair enumeration."""
         _check(_lib.maple_set_filter_algorithm(self.h, which), self.h)
 
     @property

@@ -245,20 +245,21 @@ def test_tc_and_simt_kernels_agree(gpu_lib, name):
 
 @pytest.mark.parametrize("name,N", [("C1", 1024), ("C2a", 8192), ("C2b", 8192), ("C3", 4096)])
 def test_filter_algorithms_identical(gpu_lib, name, N):
-    """The tiled and the indexed ⊑ filter enumerate different pairs but decide the same pairwise property:
-    identical kept sets (bit for bit), and G1 against the oracle on the GPU candidates for the indexed one."""
+    """The tiled, the indexed and the level-synchronous ⊑ filter enumerate different pairs but decide the same
+    pairwise property: identical kept sets (bit for bit), and G1 against the oracle on the GPU candidates."""
     from synth import config
     inst = config(name)
     ctx = _ctx(gpu_lib, inst)
     out = []
-    for algo in (1, 2):
+    for algo in (1, 2, 3):
         ctx.set_filter_algorithm(algo)
         ctx.set_debug(True)
         out.append(ctx.extract(N, inst.steps, inst.lr, inst.seed).rows())
+        if name == "C1":   # (the other shapes' G1 tests run through the auto filter)
+            ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, ctx.candidates())
+            assert nbad == 0 and [tuple(r) for r in out[-1].tolist()] == ref
     np.testing.assert_array_equal(out[0], out[1])
-    if name == "C1":   # (the other shapes' G1 tests run through the auto = indexed filter)
-        ref, nbad = OP.postprocess(inst.A, inst.l, inst.u, ctx.candidates())
-        assert nbad == 0 and [tuple(r) for r in out[1].tolist()] == ref
+    np.testing.assert_array_equal(out[0], out[2])
 
 
 @pytest.mark.parametrize("name,kernel", [("C1", TC), ("C1", SIMT), ("C2a", TC), ("C2a", SIMT), ("C3", SIMT)])

@@ -34,3 +34,24 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def minimal_only(path="gpurun_out/pool_C2b.npz"):
+    """The level-synchronous variant: g meets only the ⊑-minimal rows of smaller L1 filed under its support."""
+    z = np.load(path)
+    P = z["pool"].astype(np.int64)
+    K = z["kept"]
+    n = P.shape[1]
+    nz = P != 0
+    l1 = np.abs(P).sum(1)
+    freq = nz.sum(0)
+    key = np.where(nz, freq[None, :], np.iinfo(np.int64).max).argmin(1)
+    kept_set = {r.tobytes() for r in K}
+    kept = np.array([r.astype(np.int8).tobytes() in kept_set for r in P])
+    Lmax = int(l1.max())
+    cnt = np.zeros((n, Lmax + 2), np.int64)
+    np.add.at(cnt, (key[kept], l1[kept]), 1)
+    cum = np.concatenate([np.zeros((n, 1), np.int64), np.cumsum(cnt, 1)], 1)
+    pairs = (nz * cum[np.arange(n)[None, :], l1[:, None]]).sum(1)
+    print("minimal-only lists: kept-row pairs %.3e (mean %.0f), dominated-row upper bound %.3e"
+          % (pairs[kept].sum(), pairs[kept].mean(), pairs[~kept].sum()))
