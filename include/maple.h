@@ -132,6 +132,18 @@ int maple_extract_range(maple_ctx* ctx, int64_t n_starts, int64_t begin, int64_t
  * of maple_extract. The buffer is only read during the call. */
 int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t stride, maple_dirset** out);
 
+/* Row-sharded global ⊑ pass (Def. 1-2). With the filter off
+ * (maple_set_filter_minimal(ctx, 0)) maple_dirset_merge gives the deduped, sorted union `pool` of all ranks'
+ * local sets — identical on every rank. Each rank then decides the rows [begin, end) of `pool`:
+ * maple_dirset_keep_range writes keep_dev[i] = 1 iff row begin + i is ⊑-minimal in the whole pool (no other pool
+ * row h has h ⊑ ±g), else 0 (end - begin bytes, DEVICE buffer of the caller; synchronised). After an all-gather of
+ * the keep bytes, maple_dirset_select keeps the rows with keep_dev[i] != 0 (pool->size DEVICE bytes) and returns
+ * them as a new sorted set — equal to maple_dirset_merge with the filter on. `pool` must belong to ctx.
+ * Errors: BAD_ARG (null, foreign set, range outside [0, size]), RANGE (sum(u-l) > 1024), CUDA, OOM. Host only. */
+int maple_set_filter_minimal(maple_ctx* ctx, int32_t on);
+int maple_dirset_keep_range(maple_ctx* ctx, const maple_dirset* pool, int64_t begin, int64_t end, uint8_t* keep_dev);
+int maple_dirset_select(maple_ctx* ctx, const maple_dirset* pool, const uint8_t* keep_dev, maple_dirset** out);
+
 /* Direction-set accessors: canonical rows (first nonzero > 0), lexicographically sorted, size x n. */
 int64_t maple_dirset_size(const maple_dirset* ds);
 int64_t maple_dirset_pool_size(const maple_dirset* ds);   /* unique checked rows before the ⊑ filter */

@@ -5,7 +5,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -276,54 +275,25 @@ HashSet hashset(maple_ctx* ctx) {
                    reinterpret_cast<int*>(counters(ctx) + C_OVF), counters(ctx) + C_MAXC};
 }
 
-// check -> filter -> compact of the ctx pool (device count) -> ONE host sync -> lex sort into a new dirset.
-// Returns MAPLE_OK, or RETRY (1) when a candidate / pool buffer overflowed (the caller grows and redoes).
-constexpr int RETRY = 1;
-int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
-    cudaStream_t s = ctx->stream;
+FilterWork make_filter_work(maple_ctx* ctx, int algo) {
     const int np = ctx->n_pad;
-    const int64_t K = ctx->pool_cap;
-    CU(cudaEventRecord(ctx->ev[2], s));
-    CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
-                   ctx->nnz, ctx->dbox.as<int32_t>()};
-    if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     FilterWork fw{ctx->n, np, ctx->Lh, std::max(ctx->Wh, 1), ctx->binary, ctx->th_off.as<int32_t>(), ctx->th_c0.as<int32_t>(),
                   ctx->th_c1.as<int32_t>(), ctx->codes.as<uint32_t>(), ctx->l1.as<int32_t>(), ctx->hist.as<int32_t>(),
                   ctx->level_start.as<int32_t>(), ctx->cursor.as<int32_t>(), ctx->order.as<int32_t>(),
                   ctx->keep.as<uint8_t>(), ctx->witness.as<int32_t>(), ctx->Lh, ctx->sig.as<uint4>(),
-                  resolved_filter_algo(ctx), 0, ctx->pool.as<int8_t>(), ctx->ffreq.as<int32_t>(),
+                  algo, 0, ctx->pool.as<int8_t>(), ctx->ffreq.as<int32_t>(),
                   ctx->fkey.as<int32_t>(), ctx->fbh.as<int32_t>(), ctx->fbs.as<int32_t>(), ctx->fbc.as<int32_t>(),
                   ctx->flrow.as<int32_t>(), ctx->flsig.as<uint4>(),
                   ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1), ctx->fgc.as<int32_t>(),
-                  ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>()};
-    const unsigned long long* dpool = counters(ctx) + C_POOL;
-    CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, filter_minimal, ctx->flags.as<uint8_t>(),
-                          counters(ctx) + C_BAD, s));
-    ctx->launches++;
-    CU(cudaEventRecord(ctx->ev[3], s));
+                  ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>(), 0, 0};
+    return fw;
+}
+
+// the compacted rows in ctx->tmp_rows (count h[C_KEEP]) -> a new lexicographically sorted dirset
+int sorted_set_from_compacted(maple_ctx* ctx, const unsigned long long* h, maple_dirset** out) {
+    cudaStream_t s = ctx->stream;
+    const int np = ctx->n_pad;
     int nl = 0;
-    CU(launch_filter(dpool, K, ctx->flags.as<uint8_t>(), fw, filter_minimal, s, &nl));
-    ctx->launches += nl;
-    CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), dpool, K, np, ctx->tmp_rows.as<int8_t>(),
-                      counters(ctx) + C_KEEP, counters(ctx) + C_NZMAX, s));
-    ctx->launches++;
-    CU(cudaEventRecord(ctx->ev[4], s));
-    static const bool htrace = getenv("MAPLE_HOST_TRACE") != nullptr;
-    auto hnow = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
-    const double th0 = htrace ? hnow() : 0.0;
-    unsigned long long h[C_N];
-    int rc = read_counters(ctx, h);
-    const double th1 = htrace ? hnow() : 0.0;
-    if (rc) return rc;
-    if (h[C_RANGE]) {   // the CTA-pair kernel's f16 operands overflowed (|z| > 60000): redo this extraction on SIMT
-        ctx->tcp_range_fail = true;
-        return RETRY;
-    }
-    if (h[C_OVF] || (int64_t)h[C_MAXC] > ctx->cand_cap) {
-        ctx->want_cand = std::max<int64_t>(ctx->cand_cap, (int64_t)h[C_MAXC] + ((int64_t)h[C_MAXC] >> 2) + 1024);
-        ctx->want_pool = h[C_OVF] ? 2 * ctx->pool_cap : ctx->pool_cap;
-        return RETRY;
-    }
     const int64_t M = (int64_t)h[C_KEEP];
     maple_dirset* ds = new maple_dirset();
     ds->ctx = ctx;
@@ -338,25 +308,57 @@ int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
         delete ds;
         CU(e);
     }
-    const double th2 = htrace ? hnow() : 0.0;
     CU(ctx->sortkeys.ensure(std::max<int64_t>(M, 1) * np));
     CU(ctx->sidx0.ensure(std::max<int64_t>(M, 1) * 4));
     CU(ctx->sidx1.ensure(std::max<int64_t>(M, 1) * 4));
-    const double th3 = htrace ? hnow() : 0.0;
-    nl = 0;
     CU(launch_lex_sort(ctx->tmp_rows.as<int8_t>(), M, ctx->n, np, ctx->sortkeys.as<uint32_t>(), ctx->sidx0.as<int32_t>(),
                        ctx->sidx1.as<int32_t>(), ds->rows, s, &nl));
     ctx->launches += nl;
-    if (htrace) {
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
-        fprintf(stderr, "[maple host] finish_set: counters %.3f ms, rows alloc %.3f ms, ensure %.3f ms, sort launch %.3f ms "
-                "(M=%lld, free %.1f GB)\n", th1 - th0, th2 - th1, th3 - th2, hnow() - th3, (long long)M, fr / 1e9);
-    }
     CU(cudaEventRecord(ctx->ev[5], s));
     if (cudaEventCreateWithFlags(&ds->ready, cudaEventDisableTiming) == cudaSuccess) cudaEventRecord(ds->ready, s);
-    ctx->timings_pending = true;
     *out = ds;
+    return MAPLE_OK;
+}
+
+// check -> filter -> compact of the ctx pool (device count) -> ONE host sync -> lex sort into a new dirset.
+// Returns MAPLE_OK, or RETRY (1) when a candidate / pool buffer overflowed (the caller grows and redoes).
+constexpr int RETRY = 1;
+int finish_set(maple_ctx* ctx, int filter_minimal, maple_dirset** out) {
+    cudaStream_t s = ctx->stream;
+    const int np = ctx->n_pad;
+    const int64_t K = ctx->pool_cap;
+    CU(cudaEventRecord(ctx->ev[2], s));
+    CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
+                   ctx->nnz, ctx->dbox.as<int32_t>()};
+    if (filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
+    FilterWork fw = make_filter_work(ctx, resolved_filter_algo(ctx));
+    const unsigned long long* dpool = counters(ctx) + C_POOL;
+    CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, filter_minimal, ctx->flags.as<uint8_t>(),
+                          counters(ctx) + C_BAD, s));
+    ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[3], s));
+    int nl = 0;
+    CU(launch_filter(dpool, K, ctx->flags.as<uint8_t>(), fw, filter_minimal, s, &nl));
+    ctx->launches += nl;
+    CU(launch_compact(ctx->pool.as<int8_t>(), ctx->keep.as<uint8_t>(), dpool, K, np, ctx->tmp_rows.as<int8_t>(),
+                      counters(ctx) + C_KEEP, counters(ctx) + C_NZMAX, s));
+    ctx->launches++;
+    CU(cudaEventRecord(ctx->ev[4], s));
+    unsigned long long h[C_N];
+    int rc = read_counters(ctx, h);
+    if (rc) return rc;
+    if (h[C_RANGE]) {   // the CTA-pair kernel's f16 operands overflowed (|z| > 60000): redo this extraction on SIMT
+        ctx->tcp_range_fail = true;
+        return RETRY;
+    }
+    if (h[C_OVF] || (int64_t)h[C_MAXC] > ctx->cand_cap) {
+        ctx->want_cand = std::max<int64_t>(ctx->cand_cap, (int64_t)h[C_MAXC] + ((int64_t)h[C_MAXC] >> 2) + 1024);
+        ctx->want_pool = h[C_OVF] ? 2 * ctx->pool_cap : ctx->pool_cap;
+        return RETRY;
+    }
+    int rc2 = sorted_set_from_compacted(ctx, h, out);
+    if (rc2) return rc2;
+    ctx->timings_pending = true;
     return MAPLE_OK;
 }
 
@@ -1015,6 +1017,75 @@ int maple_dirset_merge(maple_ctx* ctx, const int8_t* rows, int64_t k, int32_t st
     if (ctx->filter_minimal && ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
     CU(cudaSetDevice(ctx->device));
     return insert_rows_and_finish(ctx, rows, k, stride, ctx->filter_minimal, out);
+}
+
+int maple_set_filter_minimal(maple_ctx* ctx, int32_t on) {
+    if (!ctx || on < 0 || on > 1) return MAPLE_ERR_BAD_ARG;
+    ctx->filter_minimal = on;
+    return MAPLE_OK;
+}
+
+namespace {
+// the rows of `pool` (a set of this context: unique, canonical, exact) as the context's hash-set pool, count M
+int load_pool(maple_ctx* ctx, const maple_dirset* pool, int filter_minimal) {
+    const int64_t M = pool->size;
+    int rc = prepare_set(ctx, 1, std::max<int64_t>(M, 1), filter_minimal);
+    if (rc) return rc;
+    const unsigned long long mm = (unsigned long long)M;
+    CU(cudaMemcpyAsync(counters(ctx) + C_POOL, &mm, sizeof(mm), cudaMemcpyHostToDevice, ctx->stream));
+    if (M > 0) CU(cudaMemcpyAsync(ctx->pool.p, pool->rows, (size_t)M * ctx->n_pad, cudaMemcpyDeviceToDevice, ctx->stream));
+    return MAPLE_OK;
+}
+}  // namespace
+
+int maple_dirset_keep_range(maple_ctx* ctx, const maple_dirset* pool, int64_t begin, int64_t end, uint8_t* keep_dev) {
+    if (ctx) g_alloc_stream = ctx->stream;
+    if (!ctx || !pool || pool->ctx != ctx || begin < 0 || end < begin || end > pool->size || (end > begin && !keep_dev))
+        return MAPLE_ERR_BAD_ARG;
+    if (ctx->Wh > 32) FAIL(MAPLE_ERR_RANGE, "⊑ filter supports sum(u-l) <= 1024");
+    if (end == begin) return MAPLE_OK;
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    int rc = load_pool(ctx, pool, 1);
+    if (rc) return rc;
+    const int np = ctx->n_pad;
+    const int64_t K = ctx->pool_cap;
+    // pairwise against every pool row of smaller L1 (not only the minimal ones: those are decided on other shards)
+    FilterWork fw = make_filter_work(ctx, ctx->n > 1024 ? 1 : 2);
+    fw.g_begin = begin;
+    fw.g_end = end;
+    CheckParams cp{ctx->m, ctx->n, np, ctx->A_rowptr.as<int32_t>(), ctx->A_col.as<int32_t>(), ctx->A_val.as<int32_t>(),
+                   ctx->nnz, ctx->dbox.as<int32_t>()};
+    const unsigned long long* dpool = counters(ctx) + C_POOL;
+    CU(launch_check_codes(ctx->pool.as<int8_t>(), dpool, K, cp, fw, 1, ctx->flags.as<uint8_t>(), counters(ctx) + C_BAD, s));
+    int nl = 0;
+    CU(launch_filter(dpool, K, ctx->flags.as<uint8_t>(), fw, 1, s, &nl));
+    ctx->launches += 1 + nl;
+    CU(cudaMemcpyAsync(keep_dev, ctx->keep.as<uint8_t>() + begin, (size_t)(end - begin), cudaMemcpyDeviceToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    return MAPLE_OK;
+}
+
+int maple_dirset_select(maple_ctx* ctx, const maple_dirset* pool, const uint8_t* keep_dev, maple_dirset** out) {
+    if (ctx) g_alloc_stream = ctx->stream;
+    if (!ctx || !pool || pool->ctx != ctx || !out || (pool->size > 0 && !keep_dev)) return MAPLE_ERR_BAD_ARG;
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    int rc = load_pool(ctx, pool, 0);
+    if (rc) return rc;
+    const unsigned long long* dpool = counters(ctx) + C_POOL;
+    CU(launch_compact(ctx->pool.as<int8_t>(), keep_dev, dpool, ctx->pool_cap, ctx->n_pad, ctx->tmp_rows.as<int8_t>(),
+                      counters(ctx) + C_KEEP, counters(ctx) + C_NZMAX, s));
+    ctx->launches++;
+    unsigned long long h[C_N];
+    rc = read_counters(ctx, h);
+    if (rc) return rc;
+    h[C_POOL] = (unsigned long long)pool->pool_size;   // the selected set reports the pool it came from
+    h[C_BAD] = 0;
+    rc = sorted_set_from_compacted(ctx, h, out);
+    if (rc) return rc;
+    CU(cudaStreamSynchronize(s));
+    return MAPLE_OK;
 }
 
 int maple_dirset_from_host(maple_ctx* ctx, const int32_t* rows, int64_t k, int32_t filter_minimal,

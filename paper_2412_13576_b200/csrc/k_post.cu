@@ -324,12 +324,12 @@ dominance_kernel(FilterWork fw) {
     const int32_t nblk = (n_valid + kFilterThreads - 1) / kFilterThreads;
     for (int32_t pb = blockIdx.x; pb < nblk; pb += gridDim.x) {
         const int32_t pos = pb * kFilterThreads + threadIdx.x;
-        const bool active0 = pos < n_valid;
-        int32_t row = -1, limit = 0;
+        int32_t row = pos < n_valid ? fw.order[pos] : -1, limit = 0;
+        // rows outside [g_begin, g_end) (a shard of the global pass; g_end = 0: all rows) are only dominators here
+        const bool active0 = row >= 0 && (fw.g_end == 0 || (row >= fw.g_begin && row < fw.g_end));
         uint32_t P[WH], N[WH];
         uint32_t fp0 = 0, fp1 = 0, fn0 = 0, fn1 = 0;
         if (active0) {
-            row = fw.order[pos];
             limit = fw.level_start[fw.l1[row]];  // rows with strictly smaller L1
 #pragma unroll
             for (int w = 0; w < WH; ++w) {

@@ -4,10 +4,12 @@ real exchange step.
 Extraction shards naturally: rank r of W owns global starts [r N / W, (r+1) N / W) (the RNG is keyed by the
 global start index, so the union of the shards' candidates equals the single-GPU candidate set). Each rank
 extracts, checks, dedupes and ⊑-filters locally (a locally non-minimal row is globally non-minimal), then
-ONE all-gather of the padded local rows (NCCL over NVLink on the GPU path) feeds the global merge
-(dedupe + ⊑ filter + lex sort) that every rank runs on the identical union, so every rank ends with the
-identical set. Augmentation incumbents are sharded the same way and the per-rank bests are all-gathered
-(f, x) with the lexicographic tie-break (reading #19).
+ONE all-gather of the padded local rows (NCCL over NVLink on the GPU path) gives every rank the identical
+union; its dedupe + lex sort (the pool) is replicated, and the global ⊑ pass is ROW-SHARDED: rank r decides
+rows shard_range(|pool|, r, W) of the pool against the whole pool (maple_dirset_keep_range), one all-gather
+of the keep bytes follows, and every rank selects the same rows (maple_dirset_select) — identical sets on
+every rank, the filter work split W ways. Augmentation incumbents are sharded the same way and the per-rank
+bests are all-gathered (f, x) with the lexicographic tie-break (reading #19).
 
 The functions take the local compute as callables so that the same exchange logic runs with NCCL on the
 GPU (product path: libmaple) and with gloo on CPU tensors in the tests.
@@ -44,6 +46,29 @@ def gather_rows(local: torch.Tensor, group=None) -> torch.Tensor:
     return torch.cat(parts, dim=0) if parts else out[:0]
 
 
+def gather_bytes(local: torch.Tensor, counts: list[int], group=None) -> torch.Tensor:
+    """All-gather 1-D uint8 tensors whose per-rank lengths `counts` every rank already knows (no count
+    exchange): one all-gather of the pieces padded to max(counts). Returns the concatenation in rank order."""
+    world = dist.get_world_size(group)
+    kmax = max(max(counts), 1)
+    pad = torch.zeros(kmax, dtype=torch.uint8, device=local.device)
+    pad[: local.shape[0]] = local
+    out = torch.empty(world * kmax, dtype=torch.uint8, device=local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return torch.cat([out[r * kmax: r * kmax + counts[r]] for r in range(world)])
+
+
+def sharded_global_pass(n_pool: int, keep_range_fn, select_fn, group=None):
+    """Row-sharded global ⊑ pass: rank r computes the keep bytes of pool rows
+    shard_range(n_pool, r, W) with keep_range_fn(begin, end) -> uint8 tensor (end - begin,), one all-gather
+    of the bytes, then select_fn(keep bytes of all n_pool rows) on every rank."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    a, e = shard_range(n_pool, rank, world)
+    keep_local = keep_range_fn(a, e)
+    counts = [shard_range(n_pool, r, world)[1] - shard_range(n_pool, r, world)[0] for r in range(world)]
+    return select_fn(gather_bytes(keep_local, counts, group))
+
+
 def best_across_ranks(x_best: np.ndarray, f_best: float, device, group=None):
     """All-gather every rank's (f, x) and return the global best (min f, ties lexicographically smallest x)."""
     world = dist.get_world_size(group)
@@ -61,33 +86,56 @@ def _on_host(group) -> bool:
     return dist.get_backend(group) == "gloo"
 
 
-def sharded_extract(ctx, n_total: int, steps: int, lr: float, seed: int, group=None):
+def sharded_extract(ctx, n_total: int, steps: int, lr: float, seed: int, group=None, shard_filter: bool = True):
     """Product path (GPU): local maple_extract_range -> all-gather (NCCL on device buffers; gloo through host
-    staging) -> maple_dirset_merge on the device. Returns (merged set, local set)."""
+    staging) -> global pass on the device: with shard_filter, the union's dedupe + sort on every rank and the
+    row-sharded ⊑ pass (sharded_global_pass); else maple_dirset_merge (dedupe + filter + sort) on every rank.
+    Returns (merged set, local set)."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     a, b = shard_range(n_total, rank, world)
     local = ctx.extract_range(n_total, a, b, steps, lr, seed)
     stride = local.stride
-    if _on_host(group):
-        host = torch.from_numpy(np.ascontiguousarray(local.rows_pinned()))          # (k, n) int8
-        if host.shape[1] < stride:
-            host = torch.nn.functional.pad(host, (0, stride - host.shape[1]))
-        rows = gather_rows(host, group)
-        if rows.shape[0] == 0:
-            return ctx.dirset_from_host(np.zeros((0, ctx.n), np.int32)), local
-        dev = rows.to(f"cuda:{ctx.device}")
+    host = _on_host(group)
+    cuda = f"cuda:{ctx.device}"
+    if host:
+        staged = torch.from_numpy(np.ascontiguousarray(local.rows_pinned()))          # (k, n) int8
+        if staged.shape[1] < stride:
+            staged = torch.nn.functional.pad(staged, (0, stride - staged.shape[1]))
+        rows = gather_rows(staged, group).to(cuda)
         torch.cuda.current_stream().synchronize()
-        return ctx.merge_device(dev.data_ptr(), dev.shape[0], stride), local
-    buf = torch.empty((max(local.size, 1), stride), dtype=torch.int8, device=f"cuda:{ctx.device}")
-    # the allocation is ordered on torch's current stream and the library copies on its own stream: drain the
-    # current stream first (the copy itself is synchronous), so no earlier use of the block can land afterwards
-    torch.cuda.current_stream().synchronize()
-    if local.size:
-        local.copy_device(buf.data_ptr())
-    rows = gather_rows(buf[: local.size], group)
-    torch.cuda.current_stream().synchronize()
-    merged = ctx.merge_device(rows.data_ptr(), rows.shape[0], stride) if rows.shape[0] else \
-        ctx.dirset_from_host(np.zeros((0, ctx.n), np.int32))
+    else:
+        buf = torch.empty((max(local.size, 1), stride), dtype=torch.int8, device=cuda)
+        # the allocation is ordered on torch's current stream and the library copies on its own stream: drain the
+        # current stream first (the copy itself is synchronous), so no earlier use of the block can land afterwards
+        torch.cuda.current_stream().synchronize()
+        if local.size:
+            local.copy_device(buf.data_ptr())
+        rows = gather_rows(buf[: local.size], group)
+        torch.cuda.current_stream().synchronize()
+    if rows.shape[0] == 0:
+        return ctx.dirset_from_host(np.zeros((0, ctx.n), np.int32)), local
+    if not shard_filter:
+        return ctx.merge_device(rows.data_ptr(), rows.shape[0], stride), local
+    ctx.set_filter_minimal(False)
+    try:
+        pool = ctx.merge_device(rows.data_ptr(), rows.shape[0], stride)   # dedupe + sort of the union
+    finally:
+        ctx.set_filter_minimal(True)
+
+    def keep_range(begin, end):
+        keep = torch.empty(max(end - begin, 1), dtype=torch.uint8, device=cuda)
+        torch.cuda.current_stream().synchronize()
+        ctx.keep_range(pool, begin, end, keep.data_ptr())
+        keep = keep[: end - begin]
+        return keep.cpu() if host else keep
+
+    def select(keep_all):
+        keep_all = keep_all.to(cuda)
+        torch.cuda.current_stream().synchronize()
+        return ctx.select(pool, keep_all.data_ptr())
+
+    merged = sharded_global_pass(pool.size, keep_range, select, group)
+    pool.free()
     return merged, local
 
 

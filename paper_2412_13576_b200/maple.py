@@ -55,6 +55,9 @@ _SIGS = [
     ("maple_dirset_copy_device", C.c_int, [_P, _P]),
     ("maple_dirset_free", None, [_P]),
     ("maple_dirset_from_host", C.c_int, [_P, _P, C.c_int64, C.c_int32, C.POINTER(_P)]),
+    ("maple_set_filter_minimal", C.c_int, [_P, C.c_int32]),
+    ("maple_dirset_keep_range", C.c_int, [_P, _P, C.c_int64, C.c_int64, _P]),
+    ("maple_dirset_select", C.c_int, [_P, _P, _P, C.POINTER(_P)]),
     ("maple_augment", C.c_int, [_P, _P, C.POINTER(maple_objective), _P, _P, C.c_int32, _P, _P, _P, _P]),
     ("maple_augment_many", C.c_int, [_P, _P, C.c_int32, C.POINTER(maple_objective), _P, _P, C.c_int32, _P, _P]),
     ("maple_debug_descent", C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_uint64, _P, _P]),
@@ -305,6 +308,20 @@ class Context:
     def merge_device(self, ptr: int, k: int, stride: int) -> DirSet:
         h = C.c_void_p()
         _check(_lib.maple_dirset_merge(self.h, C.c_void_p(ptr), int(k), int(stride), C.byref(h)), self.h)
+        return DirSet(self, h)
+
+    def set_filter_minimal(self, on: bool):
+        """maple_set_filter_minimal: whether extract / merge apply the ⊑-minimality filter (default on)."""
+        _check(_lib.maple_set_filter_minimal(self.h, int(bool(on))), self.h)
+
+    def keep_range(self, pool: DirSet, begin: int, end: int, keep_ptr: int):
+        """maple_dirset_keep_range: keep bytes of pool rows [begin, end) into the device buffer at keep_ptr."""
+        _check(_lib.maple_dirset_keep_range(self.h, pool.h, int(begin), int(end), C.c_void_p(keep_ptr)), self.h)
+
+    def select(self, pool: DirSet, keep_ptr: int) -> DirSet:
+        """maple_dirset_select: the pool rows whose keep byte (device buffer, pool.size bytes) is nonzero."""
+        h = C.c_void_p()
+        _check(_lib.maple_dirset_select(self.h, pool.h, C.c_void_p(keep_ptr), C.byref(h)), self.h)
         return DirSet(self, h)
 
     def dirset_from_host(self, rows, filter_minimal=True) -> DirSet:

@@ -1,6 +1,6 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU exchange logic in paper_2412_13576_b200/distributed.py:
-start sharding, the padded variable-count all-gather, the local-filter-then-global-merge soundness, and the
-cross-rank best with the lexicographic tie-break. The local compute is the oracle here (CPU); on the GPU the
+start sharding, the padded variable-count all-gather, the local-filter-then-global-merge soundness, the
+row-sharded global ⊑ pass (keep-byte all-gather), and the cross-rank best with the lexicographic tie-break. The local compute is the oracle here (CPU); on the GPU the
 same functions run with NCCL around libmaple (tests cannot stand in more GPUs than the one available)."""
 import os
 import socket
@@ -48,7 +48,23 @@ def _worker(rank, world, port, q):
         full_pool, _ = OX.extract_pool(B, Bp, inst.l, inst.u, N, T, 0.05, seed=4)
         out["single"] = sorted(OP.minimal_filter(full_pool))
         out["range"] = (a, b)
-        # 3) best across ranks, tie on f broken by lexicographically smallest x
+        # 3) row-sharded global ⊑ pass: keep bytes of this rank's rows of the (identical) union pool, one
+        # all-gather of the bytes, selection == the single-process minimal set
+        U = np.array(sorted(full_pool), dtype=np.int64).reshape(-1, 4)   # the deduped, sorted union
+        mins = set(OP.minimal_filter(full_pool))
+        seen = {}
+
+        def keep_fn(lo, hi):
+            seen["range"] = (lo, hi)
+            return torch.tensor([1 if tuple(int(v) for v in U[i]) in mins else 0 for i in range(lo, hi)],
+                                dtype=torch.uint8)
+
+        sel = D.sharded_global_pass(len(U), keep_fn, lambda kb: [tuple(int(v) for v in U[i])
+                                                                  for i in range(len(U)) if kb[i]])
+        out["sharded_pass"] = sorted(sel)
+        out["keep_range"] = seen["range"]
+        out["n_union"] = len(U)
+        # 4) best across ranks, tie on f broken by lexicographically smallest x
         xb = np.array([2, 0, 1, 3]) if rank == 0 else np.array([1, 2, 0, 3])
         out["best"] = D.best_across_ranks(xb, 5.0, "cpu")
         q.put((rank, out))
@@ -72,6 +88,9 @@ def test_gloo_world2_exchange():
     assert res[0]["range"] == (0, 100) and res[1]["range"] == (100, 200)
     assert res[0]["merged"] == res[1]["merged"] == res[0]["single"]
     assert len(res[0]["single"]) == 6
+    assert res[0]["sharded_pass"] == res[1]["sharded_pass"] == sorted(res[0]["single"])
+    nu = res[0]["n_union"]
+    assert res[0]["keep_range"] == (0, nu // 2) and res[1]["keep_range"] == (nu // 2, nu)
     bx, bf = res[0]["best"]
     assert bx.tolist() == [1, 2, 0, 3] and bf == 5.0
     assert res[1]["best"][0].tolist() == [1, 2, 0, 3]

@@ -2,8 +2,9 @@
 GPU available: sharded_extract / sharded_augment with NCCL at world size 1, and with gloo at world size 2 (two
 processes, each driving the same GPU with its own context; the exchange goes through host staging, so no kernel
 ever waits on another process). Both must reproduce maple_extract / maple_augment bit for bit: starts are keyed
-by their global index, a locally non-minimal row is globally non-minimal, and the merge re-runs the exact global
-dedupe + ⊑ filter + lexicographic sort."""
+by their global index, a locally non-minimal row is globally non-minimal, and the global pass re-runs the exact
+dedupe + lexicographic sort of the union and the row-sharded ⊑ filter (keep bytes per rank, one all-gather).
+The row-sharded pass itself is also checked through the C ABI with uneven shards."""
 import os
 import socket
 
@@ -96,3 +97,30 @@ def test_sharded_path_gloo_world2(gpu_lib, name, N, T):
         np.testing.assert_array_equal(rows, ref_rows)          # every rank ends with the identical global set
         assert xb == ref_x.tolist() and fb == ref_f
     assert sum(r[2] for r in res) >= len(ref_rows)            # local sets cover the global one
+
+
+@pytest.mark.parametrize("name,N,cuts", [("C2b", 8192, (0, 1, 3)), ("C3", 4096, (0, 2, 7))])
+def test_keep_range_shards_equal_merge(gpu_lib, name, N, cuts):
+    """maple_dirset_keep_range over uneven shards [b_i, b_{i+1}) of the union pool + maple_dirset_select equals
+    the filtered merge bit for bit (the keep bit is pairwise against the whole pool, so shards are independent)."""
+    from synth import config
+    inst = config(name)
+    ctx = gpu_lib.Context(inst.A, inst.l, inst.u)
+    ref = ctx.extract(N, inst.steps, inst.lr, inst.seed)
+    ctx.set_filter_minimal(False)
+    raw = ctx.extract(N, inst.steps, inst.lr, inst.seed)          # the unfiltered (deduped, sorted) pool
+    buf = torch.empty((max(raw.size, 1), raw.stride), dtype=torch.int8, device="cuda:0")
+    torch.cuda.synchronize()
+    raw.copy_device(buf.data_ptr())
+    pool = ctx.merge_device(buf.data_ptr(), raw.size, raw.stride)   # a union as the ranks would gather it
+    ctx.set_filter_minimal(True)
+    assert pool.size == raw.size == ref.pool_size
+    M = pool.size
+    bounds = [M * c // 8 for c in cuts] + [M]
+    keep = torch.zeros(M, dtype=torch.uint8, device="cuda:0")
+    torch.cuda.synchronize()
+    for a, b in zip(bounds[:-1], bounds[1:]):
+        ctx.keep_range(pool, a, b, keep.data_ptr() + a)
+    assert int(keep.sum().item()) == ref.size
+    sel = ctx.select(pool, keep.data_ptr())
+    np.testing.assert_array_equal(sel.rows(), ref.rows())
