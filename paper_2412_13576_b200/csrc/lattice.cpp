@@ -9,6 +9,7 @@
 //   B+ = (B^T B)^{-1} B^T (Remark P:321-324): exact Gram matrix, fp64 Cholesky solve.
 // Independent of oracle/lattice.py (which uses Python big integers and a different LLL bookkeeping).
 #include <algorithm>
+#include <immintrin.h>
 #include <cmath>
 #include <cstdint>
 #include <string>
@@ -50,29 +51,38 @@ inline i128 iabs(i128 a) { return a < 0 ? -a : a; }
 }  // namespace
 
 int host_kernel_basis(const int32_t* A, int m, int n, std::vector<int64_t>& B, std::string& err) {
-    // M: m x n working copy (row-major), C: n x n (row-major), columns are what we operate on.
+    // Column-major working copies: M (m x n) and C (n x n), column j contiguous, so a column operation streams
+    // two contiguous columns; C starts as the identity and stays sparse, and zero entries of the source column
+    // are skipped (no checked multiply), which keeps the operation count near the nonzeros touched.
     std::vector<i128> M(size_t(m) * n), C(size_t(n) * n, 0);
-    for (int i = 0; i < m * n; ++i) M[i] = A[i];
+    for (int r = 0; r < m; ++r)
+        for (int j = 0; j < n; ++j) M[size_t(j) * m + r] = A[size_t(r) * n + j];
     for (int i = 0; i < n; ++i) C[size_t(i) * n + i] = 1;
+    auto mcol = [&](int j) { return &M[size_t(j) * m]; };
+    auto ccol = [&](int j) { return &C[size_t(j) * n]; };
     auto axpy = [&](int j, int p, i128 q) {  // col_j -= q col_p
         if (q == 0) return;
-        for (int r = 0; r < m; ++r) M[size_t(r) * n + j] = sub_chk(M[size_t(r) * n + j], mul_chk(q, M[size_t(r) * n + p]));
-        for (int r = 0; r < n; ++r) C[size_t(r) * n + j] = sub_chk(C[size_t(r) * n + j], mul_chk(q, C[size_t(r) * n + p]));
+        i128 *mj = mcol(j), *cj = ccol(j);
+        const i128 *mp = mcol(p), *cp = ccol(p);
+        for (int r = 0; r < m; ++r)
+            if (mp[r] != 0) mj[r] = sub_chk(mj[r], mul_chk(q, mp[r]));
+        for (int r = 0; r < n; ++r)
+            if (cp[r] != 0) cj[r] = sub_chk(cj[r], mul_chk(q, cp[r]));
     };
     auto cswap = [&](int a, int b) {
         if (a == b) return;
-        for (int r = 0; r < m; ++r) std::swap(M[size_t(r) * n + a], M[size_t(r) * n + b]);
-        for (int r = 0; r < n; ++r) std::swap(C[size_t(r) * n + a], C[size_t(r) * n + b]);
+        std::swap_ranges(mcol(a), mcol(a) + m, mcol(b));
+        std::swap_ranges(ccol(a), ccol(a) + n, ccol(b));
     };
+    auto Mrc = [&](int r, int j) -> i128& { return M[size_t(j) * m + r]; };
     try {
         for (int i = 0; i < m; ++i) {
-            const i128* row = &M[size_t(i) * n];
             for (;;) {
                 int p = -1, cnt = 0;
                 for (int j = i; j < n; ++j)
-                    if (row[j] != 0) {
+                    if (Mrc(i, j) != 0) {
                         ++cnt;
-                        if (p < 0 || iabs(row[j]) < iabs(row[p])) p = j;
+                        if (p < 0 || iabs(Mrc(i, j)) < iabs(Mrc(i, p))) p = j;
                     }
                 if (cnt == 0) {
                     err = "rank(A) < m: row " + std::to_string(i) + " has no pivot";
@@ -83,13 +93,14 @@ int host_kernel_basis(const int32_t* A, int m, int n, std::vector<int64_t>& B, s
                     break;
                 }
                 for (int j = i; j < n; ++j)
-                    if (j != p && row[j] != 0) axpy(j, p, fdiv(row[j], row[p]));
+                    if (j != p && Mrc(i, j) != 0) axpy(j, p, fdiv(Mrc(i, j), Mrc(i, p)));
             }
-            if (M[size_t(i) * n + i] < 0) {
-                for (int r = 0; r < m; ++r) M[size_t(r) * n + i] = -M[size_t(r) * n + i];
-                for (int r = 0; r < n; ++r) C[size_t(r) * n + i] = -C[size_t(r) * n + i];
+            if (Mrc(i, i) < 0) {
+                for (int r = 0; r < m; ++r) mcol(i)[r] = -mcol(i)[r];
+                for (int r = 0; r < n; ++r) ccol(i)[r] = -ccol(i)[r];
             }
-            for (int j = 0; j < i; ++j) axpy(j, i, fdiv(M[size_t(i) * n + j], M[size_t(i) * n + i]));
+            for (int j = 0; j < i; ++j)
+                if (Mrc(i, j) != 0) axpy(j, i, fdiv(Mrc(i, j), Mrc(i, i)));
         }
     } catch (Overflow&) {
         err = "integer overflow in HNF (checked __int128)";
@@ -97,15 +108,16 @@ int host_kernel_basis(const int32_t* A, int m, int n, std::vector<int64_t>& B, s
     }
     const int d = n - m;
     B.assign(size_t(n) * d, 0);
-    for (int r = 0; r < n; ++r)
-        for (int j = 0; j < d; ++j) {
-            i128 v = C[size_t(r) * n + m + j];
-            if (v > INT64_MAX || v < INT64_MIN) {
-                err = "kernel basis entry exceeds int64";
-                return -5;
+    for (int j0 = 0; j0 < d; j0 += 16)   // blocked transpose: 16 contiguous columns of C -> 16 adjacent entries of B
+        for (int r = 0; r < n; ++r)
+            for (int j = j0; j < std::min(d, j0 + 16); ++j) {
+                const i128 v = C[size_t(m + j) * n + r];
+                if (v > INT64_MAX || v < INT64_MIN) {
+                    err = "kernel basis entry exceeds int64";
+                    return -5;
+                }
+                B[size_t(r) * d + j] = (int64_t)v;
             }
-            B[size_t(r) * d + j] = (int64_t)v;
-        }
     return 0;
 }
 
@@ -113,7 +125,7 @@ namespace {
 
 // 4 independent accumulators (ILP / vectorisation); the sum of exact integer products is exact in double
 // while every partial sum stays below 2^53 (guaranteed by the caller's entry bound)
-inline double dot4(const double* a, const double* b, int len) {
+inline double dot4_scalar(const double* a, const double* b, int len) {
     double s0 = 0, s1 = 0, s2 = 0, s3 = 0;
     int r = 0;
     for (; r + 4 <= len; r += 4) {
@@ -124,6 +136,33 @@ inline double dot4(const double* a, const double* b, int len) {
     }
     for (; r < len; ++r) s0 += a[r] * b[r];
     return (s0 + s1) + (s2 + s3);
+}
+
+// the same dot product with 4 x 4 AVX2 FMA lanes, chosen at run time when the host CPU has AVX2 + FMA (the
+// library is built for baseline x86-64); a different summation order than the scalar version — equally valid
+// for the fp64 Gram-Schmidt data and Cholesky factors (exact integer sums stay exact either way)
+__attribute__((target("avx2,fma"))) double dot4_avx2(const double* a, const double* b, int len) {
+    __m256d s0 = _mm256_setzero_pd(), s1 = _mm256_setzero_pd(), s2 = _mm256_setzero_pd(), s3 = _mm256_setzero_pd();
+    int r = 0;
+    for (; r + 16 <= len; r += 16) {
+        s0 = _mm256_fmadd_pd(_mm256_loadu_pd(a + r), _mm256_loadu_pd(b + r), s0);
+        s1 = _mm256_fmadd_pd(_mm256_loadu_pd(a + r + 4), _mm256_loadu_pd(b + r + 4), s1);
+        s2 = _mm256_fmadd_pd(_mm256_loadu_pd(a + r + 8), _mm256_loadu_pd(b + r + 8), s2);
+        s3 = _mm256_fmadd_pd(_mm256_loadu_pd(a + r + 12), _mm256_loadu_pd(b + r + 12), s3);
+    }
+    for (; r + 4 <= len; r += 4) s0 = _mm256_fmadd_pd(_mm256_loadu_pd(a + r), _mm256_loadu_pd(b + r), s0);
+    const __m256d t = _mm256_add_pd(_mm256_add_pd(s0, s1), _mm256_add_pd(s2, s3));
+    alignas(32) double v[4];
+    _mm256_store_pd(v, t);
+    double acc = (v[0] + v[1]) + (v[2] + v[3]);
+    for (; r < len; ++r) acc += a[r] * b[r];
+    return acc;
+}
+
+const bool kHaveAvx2 = __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma");
+
+inline double dot4(const double* a, const double* b, int len) {
+    return kHaveAvx2 ? dot4_avx2(a, b, len) : dot4_scalar(a, b, len);
 }
 
 // LLL fast path: the same algorithm as the exact path below (size reduction against j = k-1..0, Siegel test,
@@ -143,16 +182,34 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
         }
     std::vector<double> mu((size_t)d * d, 0.0), rr((size_t)d * d, 0.0), Bs(d, 0.0);
     auto col = [&](int k) { return &b[(size_t)k * n]; };
-    // nonzero rows of every column (kernel bases are sparse: C5 has ~4 nonzeros per column of 1000), so the inner
-    // products of Gram-Schmidt cost O(nnz) instead of O(n); refreshed whenever a column changes
-    std::vector<std::vector<int>> nz(d);
-    auto refresh = [&](int k) {
+    // nonzero rows of every column (kernel bases are sparse: C5 has ~4 nonzeros per column of 1000) and, per row,
+    // the columns nonzero there: the Gram row <b_k, b_j> (j < k) then costs the actual column overlaps only
+    std::vector<std::vector<int>> nz(d), rc(n);
+    auto unlink = [&](int k) {
+        for (int r : nz[k]) {
+            auto& v = rc[r];
+            for (size_t t = 0; t < v.size(); ++t)
+                if (v[t] == k) {
+                    v[t] = v.back();
+                    v.pop_back();
+                    break;
+                }
+        }
+    };
+    auto link = [&](int k) {
         nz[k].clear();
         const double* c = col(k);
         for (int r = 0; r < n; ++r)
-            if (c[r] != 0.0) nz[k].push_back(r);
+            if (c[r] != 0.0) {
+                nz[k].push_back(r);
+                rc[r].push_back(k);
+            }
     };
-    for (int k = 0; k < d; ++k) refresh(k);
+    auto refresh = [&](int k) {
+        unlink(k);
+        link(k);
+    };
+    for (int k = 0; k < d; ++k) link(k);
     auto sdot = [&](int a, int c) {   // exact: integer products and partial sums below 2^53
         const std::vector<int>& s = nz[a].size() <= nz[c].size() ? nz[a] : nz[c];
         const double *x = col(a), *y = col(c);
@@ -160,26 +217,32 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
         for (int r : s) acc += x[r] * y[r];
         return acc;
     };
-    // row k of the Gram-Schmidt data: r_kj = <b_k, b_j> - sum_{l<j} mu_jl r_kl. The sum runs over the nonzero
-    // r_kl only (skipping exact zeros leaves every partial sum unchanged), so a sparse, nearly orthogonal basis
-    // costs O(nnz) per row instead of O(k^2)
-    std::vector<int> rnz;
-    rnz.reserve(d);
+    // row k of the Gram-Schmidt data: r_kj = <b_k, b_j> - sum_{l<j} mu_jl r_kl, as a dense unit-triangular
+    // recurrence over the contiguous rows of mu (vectorised dot products), starting at the first j whose Gram
+    // entry is nonzero (r_kj = 0 before it)
+    std::vector<double> gk(d, 0.0);
+    std::vector<int> touched;
     auto gso_row = [&](int k) {
         double* rk = &rr[(size_t)k * d];
         double* mk = &mu[(size_t)k * d];
-        rnz.clear();
-        for (int j = 0; j < k; ++j) {
-            const double* mj = &mu[(size_t)j * d];
-            double s = sdot(k, j);
-            for (int l : rnz) s -= mj[l] * rk[l];
+        touched.clear();
+        const double* xk = col(k);
+        int f = k;
+        for (int r : nz[k])
+            for (int j : rc[r])
+                if (j < k) {
+                    if (gk[j] == 0.0) touched.push_back(j);
+                    gk[j] += xk[r] * col(j)[r];   // exact integers
+                    f = std::min(f, j);
+                }
+        for (int j = 0; j < f; ++j) rk[j] = mk[j] = 0.0;
+        for (int j = f; j < k; ++j) {
+            const double s = gk[j] - dot4(&mu[(size_t)j * d + f], rk + f, j - f);
             rk[j] = s;
             mk[j] = s / Bs[j];
-            if (s != 0.0) rnz.push_back(j);
         }
-        double s = sdot(k, k);
-        for (int l : rnz) s -= mk[l] * rk[l];
-        Bs[k] = s;
+        for (int j : touched) gk[j] = 0.0;
+        Bs[k] = sdot(k, k) - dot4(mk + f, rk + f, k - f);
     };
     gso_row(0);
     if (Bs[0] <= 0) {
@@ -219,8 +282,11 @@ int lll_fast(std::vector<int64_t>& Bnd, int n, int d, std::string& err) {
             return -3;
         }
         if (Bs[k - 1] > 2.0 * Bs[k] * (1.0 + 1e-12)) {  // Siegel test (Alg. 1 line 5)
+            unlink(k);
+            unlink(k - 1);
             std::swap_ranges(col(k), col(k) + n, col(k - 1));
-            std::swap(nz[k], nz[k - 1]);
+            link(k);
+            link(k - 1);
             gso_row(k - 1);
             k = (k - 1 > 1) ? k - 1 : 1;
             if (k == 1) gso_row(0);
@@ -396,13 +462,22 @@ int pinv_fast(const std::vector<int64_t>& B, int n, int d, std::vector<double>& 
     });
     for (int a = 0; a < d; ++a)
         for (int b = 0; b < a; ++b) Ginv[(size_t)b * d + a] = Ginv[(size_t)a * d + b];
-    Bp.assign((size_t)d * n, 0.0);
-    for (int c = 0; c < n; ++c)
+    // column c of B+ = sum over row c's nonzeros (j, v) of v * column j of G^{-1}: accumulated contiguously as
+    // row c of B+^T (one thread per c), then transposed in 32 x 32 blocks
+    std::vector<double> BpT((size_t)n * d, 0.0);
+    parallel_for(n, [&](int c) {
+        double* out = &BpT[(size_t)c * d];
         for (const auto& e : rows[c]) {
             const double v = (double)e.second;
             const double* g = &Ginv[(size_t)e.first * d];   // column e.first of the symmetric G^{-1}
-            for (int i = 0; i < d; ++i) Bp[(size_t)i * n + c] += v * g[i];
+            for (int i = 0; i < d; ++i) out[i] += v * g[i];
         }
+    });
+    Bp.assign((size_t)d * n, 0.0);
+    for (int c0 = 0; c0 < n; c0 += 32)
+        for (int i0 = 0; i0 < d; i0 += 32)
+            for (int i = i0; i < std::min(d, i0 + 32); ++i)
+                for (int c = c0; c < std::min(n, c0 + 32); ++c) Bp[(size_t)i * n + c] = BpT[(size_t)c * d + i];
     return 0;
 }
 
