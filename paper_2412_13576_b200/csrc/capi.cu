@@ -203,6 +203,8 @@ int read_counters(maple_ctx* ctx, unsigned long long* h) {
     return MAPLE_OK;
 }
 
+constexpr int kGlEntriesPerRow = 32;   // G-list capacity per pool row (the level pass's support entries) ...
+constexpr size_t kGlMaxEntries = size_t(64) << 20;   // ... up to 256 MB (beyond: the indexed pass, same keep set)
 constexpr int kAutoFilter = 3;   // auto choice of the ⊑ filter's pair enumeration (n <= 1024)
 
 // the ⊑ filter's pair enumeration: 1 tiled, 2 tiled prefix + key-coordinate index, 3 tiled prefix + level-synchronous
@@ -259,7 +261,7 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap, int filter_m
         if (filter_minimal && resolved_filter_algo(ctx) == 3) {
             CU(ctx->fgc.ensure(nbins * 4));
             CU(ctx->fgs.ensure((nbins + 1) * 4));
-            CU(ctx->fgr.ensure((size_t)ctx->pool_cap * ctx->n * 4));
+            CU(ctx->fgr.ensure(std::min<size_t>((size_t)ctx->pool_cap * std::min(ctx->n, kGlEntriesPerRow), kGlMaxEntries) * 4));
             CU(ctx->fhf.ensure((size_t)ctx->n * 4 + 8));   // + the level kernel's grid barrier words
         }
     }
@@ -285,7 +287,8 @@ FilterWork make_filter_work(maple_ctx* ctx, int algo) {
                   ctx->fkey.as<int32_t>(), ctx->fbh.as<int32_t>(), ctx->fbs.as<int32_t>(), ctx->fbc.as<int32_t>(),
                   ctx->flrow.as<int32_t>(), ctx->flsig.as<uint4>(),
                   ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1), ctx->fgc.as<int32_t>(),
-                  ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>(), 0, 0};
+                  ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>(),
+                  (int64_t)(ctx->fgr.bytes / 4), 0, 0, 0};
     return fw;
 }
 
@@ -785,6 +788,7 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->ell_pos_z, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->sig, &ctx->ffreq, &ctx->fkey, &ctx->fbh, &ctx->fbs, &ctx->fbc, &ctx->flrow, &ctx->flsig, &ctx->l1,
+                      &ctx->fgc, &ctx->fgs, &ctx->fgr, &ctx->fhf,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
                       &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,

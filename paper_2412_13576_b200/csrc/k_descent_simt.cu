@@ -8,8 +8,8 @@
 //                                                  and the Adam state (m, v) of those coordinates in registers)
 // Both run from lane-major, bank-conflict-scheduled ELL words staged once per block in shared memory
 // (sparse_ell.h): per slot a warp reads one 128-byte line of words and gathers one conflict-free wavefront.
-// Per warp, shared memory holds z, the gradient Γ (reused for the rounded iterate r after Adam) and s (reused
-// for the harvested g row), so warps stay small (about 3.6 KB at C3) and 16-32 of them fit per SM.
+// Per warp, shared memory holds z, s (reused for the harvested g row) and the ELL result queue (which also holds
+// the gradient Γ); the harvest gathers round(z) straight from z. Warps stay small (about 3 KB at C3, 12 KB at C5).
 // Per start, Algorithm 3 lines 4-10:
 //   z0 = B+ g0, g0 ~ U(l-u, u-l) (counter RNG, fp64)
 //   for t = 1..T:  grad = B^T sign(B z) + lam1 (ceil z + floor z - 2z) + lam2-term   (Eq. 3)
@@ -33,6 +33,8 @@ namespace {
 #ifndef MAPLE_ELL_BATCH
 #define MAPLE_ELL_BATCH 8
 #endif
+// ROUND: gather round_half_away(x) instead of x (the harvest's g = B round(z) straight from z)
+template <bool ROUND = false>
 __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slots, const float* __restrict__ x,
                                         float* __restrict__ resq) {
     const char* xb = reinterpret_cast<const char*>(x);
@@ -48,7 +50,10 @@ __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slo
 #pragma unroll
         for (int k = 0; k < NB; ++k) w[k] = wl[(e + k) * 32];
 #pragma unroll
-        for (int k = 0; k < NB; ++k) xv[k] = *reinterpret_cast<const float*>(xb + (w[k] & 0xFFFCu));
+        for (int k = 0; k < NB; ++k) {
+            xv[k] = *reinterpret_cast<const float*>(xb + (w[k] & 0xFFFCu));
+            if (ROUND) xv[k] = round_half_away_f(xv[k]);
+        }
 #pragma unroll
         for (int k = 0; k < NB; ++k) {
             acc = fmaf(__uint_as_float(w[k] & 0xFFFF0000u), xv[k], acc);
@@ -63,7 +68,8 @@ __device__ __forceinline__ void ell_run(const uint32_t* __restrict__ wl, int slo
 #pragma unroll 4
     for (; e < slots; ++e) {
         const uint32_t w = wl[e * 32];
-        const float xv = *reinterpret_cast<const float*>(xb + (w & 0xFFFCu));
+        float xv = *reinterpret_cast<const float*>(xb + (w & 0xFFFCu));
+        if (ROUND) xv = round_half_away_f(xv);
         acc = fmaf(__uint_as_float(w & 0xFFFF0000u), xv, acc);   // bf16 B entry; PAD words carry 0
         if (w & 1u) {
             *resq = acc;
@@ -115,15 +121,14 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     // (at least one row of B+ in fp64: the start computation stages B+ here before the schedules are loaded)
     const int shared_words = max((Lf + Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1), 2 * n);
 
-    // per warp, in owner order (sparse_ell.h / capi): z [QD*32] | r after Adam [QD*32] | s, then the g row
-    // [qf*32 + nfix] | result queue; during the start computation g0 (n doubles) sits behind z
-    // (per_warp_words >= QD*32 + 2n)
+    // per warp, in owner order (sparse_ell.h / capi): z [QD*32] | s, then the g row [qf*32 + nfix] | result
+    // queue; during the start computation g0 (n doubles) sits behind z (per_warp_words >= QD*32 + 2n). The
+    // harvest gathers round(z) straight from z, so no rounded copy of the iterate is kept.
     const int s_words = sb.qf * 32 + sb.nfix;
     float* zsh = reinterpret_cast<float*>(smem_raw) + shared_words + (size_t)wid * per_warp_words;
-    float* grsh = zsh + QD * 32;
-    float* ssh = grsh + QD * 32;
+    float* ssh = zsh + QD * 32;
     float* res = ssh + s_words;
-    double* g0sh = reinterpret_cast<double*>(grsh);   // shared_words, per_warp_words and QD*32 are even
+    double* g0sh = reinterpret_cast<double*>(ssh);   // shared_words, per_warp_words and QD*32 are even
 
     const int64_t local = (int64_t)blockIdx.x * nwarps + wid;
     const bool active = local < p.count;
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     for (int k = threadIdx.x; k < n; k += blockDim.x) poss[k] = sb.pos_s[k];
     __syncthreads();
     if (!active) return;
-    for (int k = QD * 32 + lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // g0 is dead: clear r, s, queue
+    for (int k = QD * 32 + lane; k < per_warp_words; k += 32) zsh[k] = 0.f;   // g0 is dead: clear s, queue
     __syncwarp();
     const int* jq = ownb + lane;   // jq[q * 32]: this lane's q-th coordinate (shared table, conflict-free)
     const uint32_t* wf = ellf + lane;
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
         __syncwarp();
         // backward: Γ = B^T s; the lane's q-th piece is its q-th coordinate, left in its own queue slot
         ell_run(wb, Lb, ssh, res + lane);
-        // penalties + Adam (reading #9) on this lane's coordinates; r = round(z) replaces Γ in grsh.
+        // penalties + Adam (reading #9) on this lane's coordinates.
         // Branch-free: unused places update the scratch coordinate d (Γ = 0, z = 0: it stays 0).
         const float4 st = p.step_tab[t];
         // the first iterate is always harvested (no previous round(z)); final-only mode (reading #25): the last
@@ -264,14 +269,13 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             zsh[pl] = zn;
             const float rn = round_half_away_f(zn);
             changed |= rn != ro;
-            grsh[pl] = rn;
         }
         __syncwarp();
         if (!p.harvest || (p.harvest_final && !final_step)) continue;
         // harvest (Alg. 3 lines 9-10) when round(z) changed: g = B r, box, g != 0, canonical sign
         if (!__any_sync(0xffffffffu, changed)) continue;
         bool ok = true;
-        ell_run(wf, Lf, grsh, res + lane);
+        ell_run<true>(wf, Lf, zsh, res + lane);   // g = B round(z)
         ell_rows(sb, ownf, fix, fixpos, res, lane, [&](int pl, int i, float acc) {
             const int gv = (int)acc;
             ok &= (abs(gv) <= p.box[i]);
@@ -309,7 +313,7 @@ cudaError_t launch_qd(const DescentParams& p, cudaStream_t s) {
     const SparseB& sb = p.sb;
     const int n = p.n;
     const int per_warp_words =
-        (std::max(2 * QD * 32 + sb.qf * 32 + sb.nfix + 32 * std::max(sb.qf, QD), QD * 32 + 2 * n) + 1) & ~1;
+        (std::max(QD * 32 + sb.qf * 32 + sb.nfix + 32 * std::max(sb.qf, QD), QD * 32 + 2 * n) + 1) & ~1;
     const size_t shared_bytes =
         (size_t)std::max((sb.Lf + sb.Lb + sb.qf + QD) * 32 + ((3 * sb.nfix + sb.nfixpos + n + 1) & ~1), 2 * n) * 4;
     int dev = 0, smem_sm = 0, smem_blk = 0;

@@ -400,6 +400,11 @@ dominance_kernel(FilterWork fw) {
     }
 }
 
+// level-synchronous pass (algo 3, below): (the G lists' total is gl_start[(Lmax + 1) n] once scanned; beyond gl_cap the indexed pass runs instead)
+__device__ __forceinline__ bool gl_overflow(const FilterWork& fw) {
+    return (int64_t)fw.gl_start[(size_t)(fw.Lmax + 1) * fw.n] > fw.gl_cap;
+}
+
 // ---- indexed filter (large pools) ----
 // h ⊑ ±g requires supp(h) ⊆ supp(g). Every valid row h is filed under one key coordinate κ(h) ∈ supp(h) — its
 // rarest coordinate over the pool (ties: lowest index) — and, inside that list, by its L1 norm: bin
@@ -490,7 +495,7 @@ __global__ void __launch_bounds__(1024) bin_scan_kernel(FilterWork fw, int nb) {
 }
 
 __global__ void bin_scatter_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap) {
-    if (*fw.n_undec == 0) return;
+    if (*fw.n_undec == 0 || (fw.idx_fallback && !gl_overflow(fw))) return;
     const int64_t count = dev_count(dcount, cap);
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
         if (fw.l1[r] < 0) continue;
@@ -509,7 +514,7 @@ constexpr int kIdxThreads = 256;
 template <int WH>
 __global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork fw, const unsigned long long* dcount,
                                                                    int64_t cap) {
-    if (*fw.n_undec == 0) return;
+    if (*fw.n_undec == 0 || (fw.idx_fallback && !gl_overflow(fw))) return;
     __shared__ uint32_t gcode[kIdxThreads / 32][2 * WH];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int Wh = fw.Wh, W2 = 2 * Wh;
@@ -598,6 +603,7 @@ constexpr int kLvThreads = 256, kLvTile = 512, kLvSeg = 4096;
 // pass 0 counts (gl_cursor as histogram), pass 1 scatters (gl_cursor as cursor)
 __global__ void glist_kernel(FilterWork fw, const unsigned long long* dcount, int64_t cap, int pass) {
     if (*fw.n_undec == 0) return;
+    if (pass == 1 && gl_overflow(fw)) return;
     const int64_t count = dev_count(dcount, cap);
     const int nw = fw.n_pad / 16, n = fw.n;
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += (int64_t)gridDim.x * blockDim.x) {
@@ -846,7 +852,7 @@ __device__ __forceinline__ void grid_barrier(unsigned* count, unsigned* gen) {
 // barriers — after every lower level's appends, before its own — and appends need no barrier of their own (a
 // coordinate's list order is irrelevant). Returns at once when the tiled prefix decided every row.
 __global__ void __launch_bounds__(kLvThreads) level_filter_kernel(FilterWork fw, unsigned* bar) {
-    if (*fw.n_undec == 0) return;
+    if (*fw.n_undec == 0 || gl_overflow(fw)) return;
     const int n = fw.n;
     for (int L = 1; L <= fw.Lmax; ++L) {
         if (fw.level_start[L] == fw.level_start[L + 1]) continue;   // no row has L1 = L
@@ -1140,6 +1146,17 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
         if ((e = cudaLaunchCooperativeKernel((void*)level_filter_kernel, grid, kLvThreads, args, 0, s)) != cudaSuccess)
             return e;
         *launches += 1;
+        // the indexed pass instead, when the G lists did not fit (its kernels return at once otherwise)
+        fw.idx_fallback = 1;
+        bin_scatter_kernel<<<grid_for(cap), 256, 0, s>>>(fw, dcount, cap);
+        const unsigned iblocks = grid_for((cap + 7) / 8, kIdxThreads, 148 * 8);
+#define MAPLE_IDX3(WHV)                                                                 \
+        if (fw.Wh <= WHV) {                                                             \
+            dominance_idx_kernel<WHV><<<iblocks, kIdxThreads, 0, s>>>(fw, dcount, cap); \
+        } else
+        MAPLE_IDX3(2) MAPLE_IDX3(8) MAPLE_IDX3(32) return cudaErrorInvalidValue;
+#undef MAPLE_IDX3
+        *launches += 2;
         return cudaGetLastError();
     }
     if (algo == 2) {   // rows the prefix did not decide: indexed by key coordinate and L1

@@ -133,6 +133,8 @@ struct FilterWork {
     int32_t* gl_start;            // (Lmax + 1) n + 1
     int32_t* gl_rows;             // sum of |supp| over the undecided rows (capacity count x n)
     int32_t* h_fill;              // n: minimal rows appended so far to each key coordinate's list
+    int64_t gl_cap;               // capacity of gl_rows; the level pass falls back to the indexed pass beyond it
+    int idx_fallback;             // 1: the indexed-pass kernels run only when the G lists overflowed (algo 3)
     int64_t g_begin, g_end;       // decide keep only for rows [g_begin, g_end) (a shard of the global pass); g_end = 0: all
 };
 // flags[r] = 1 iff A g = 0 (exact int64), g != 0 and |g| <= u - l (conditions C1-C3), for the first

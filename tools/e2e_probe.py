@@ -1,41 +1,33 @@
-"""Host wall-clock breakdown of one end-to-end solve through the public API (create, extract, D2H, augment,
-close), repeated; used to locate host-side overhead in bench.py's e2e number. GPU box only."""
+"""Fresh-context extractions at C3 (the bench's e2e pattern): host time, device phases and kernel launches per
+call, to separate allocation / retry costs from the device work."""
+import os
 import sys
 import time
 
-import numpy as np
-import torch
-
-sys.path.insert(0, ".")
-from paper_2412_13576_b200 import maple  # noqa: E402
-from synth import config, feasible_points  # noqa: E402
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def main(name="C2a", reps=6):
-    inst = config(name)
-    X0 = feasible_points(inst, 100, seed=99)
+def main():
+    import torch
+    from paper_2412_13576_b200 import maple
+    from synth import c3
+    inst = c3()
+    maple.load()
     stream = torch.cuda.Stream()
-    torch.cuda.synchronize()
-    for r in range(reps):
-        t = [time.perf_counter()]
-        c = maple.Context(inst.A, inst.l, inst.u)
-        t.append(time.perf_counter())
-        c.set_stream(stream.cuda_stream)
-        d = c.extract(inst.n_starts if name != "C3" else 65536, inst.steps, inst.lr, inst.seed)
-        t.append(time.perf_counter())
-        rows = d.rows()
-        t.append(time.perf_counter())
-        c.augment(d, inst.Q, inst.c, inst.c0, inst.b, X0)
+    for it in range(5):
+        t0 = time.perf_counter()
+        ctx = maple.Context(inst.A, inst.l, inst.u)
+        ctx.set_stream(stream.cuda_stream)
+        t1 = time.perf_counter()
+        ds = ctx.extract(inst.n_starts, inst.steps, inst.lr, inst.seed)
         torch.cuda.synchronize()
-        t.append(time.perf_counter())
-        d.free()
-        c.close()
-        torch.cuda.synchronize()
-        t.append(time.perf_counter())
-        dt = np.diff(t) * 1e3
-        print(f"{name} rep {r}: create {dt[0]:.2f} extract {dt[1]:.2f} rows {dt[2]:.2f} augment {dt[3]:.2f} "
-              f"close {dt[4]:.2f} ms  (rows {rows.shape[0]})", flush=True)
+        t2 = time.perf_counter()
+        free, total = torch.cuda.mem_get_info()
+        print(f"iter {it}: create {1e3*(t1-t0):.1f} ms extract {1e3*(t2-t1):.1f} ms launches {ctx.launches()} "
+              f"rows {ds.size} free {free/1e9:.1f} GB timings {ctx.timings()}", flush=True)
+        ds.free()
+        ctx.close()
 
 
 if __name__ == "__main__":
-    main(*(sys.argv[1:2] or ["C2a"]))
+    main()
