@@ -3,6 +3,7 @@
 // does the once-per-A exact lattice work of maple_create (lattice.cpp) and argument validation.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 
 #include <algorithm>
 #include <cmath>
@@ -123,6 +124,8 @@ struct maple_ctx {
     // workspace
     DevBuf ffreq, fkey, fbh, fbs, fbc, flrow, flsig;   // indexed filter (k_post.cu)
     DevBuf fgc, fgs, fgr, fhf;                         // level-synchronous filter: G lists, list fill counters
+    DevBuf g0buf, z0buf;          // SIMT starts by DGEMM: g0 (chunk x n) and z0 = B+ g0 (chunk x d), fp64
+    cublasHandle_t cublas = nullptr;
     DevBuf step_tab, cand, keys, idx, pool, counters, flags, codes, sig, l1, hist, level_start, cursor, order, keep,
         witness, tmp_rows, sortkeys, sidx0, sidx1, zout, z0out;
     DevBuf aQ, ac, ac0, aqg, aX, aF2, aIt, axb, af2b, atab, atoff;
@@ -591,12 +594,51 @@ int ensure_descent_operands(maple_ctx* ctx) {
     return MAPLE_OK;
 }
 
+// The SIMT kernel computes z0 = B+ g0 per warp (fp64, a fixed-order reduction) — cheap for small n d, but at C5
+// (n d = 900,000 fp64 FMAs per start) it is a quarter of the kernel. Above this size the starts of a launch are one
+// cuBLAS DGEMM Z0 = G0 B+^T (a plain library GEMM on the fp64 tensor cores) in chunks, and the kernel reads them.
+constexpr int64_t kGemmStartsMinND = 200000;
+constexpr int64_t kGemmStartsChunk = 65536;
+
+cudaError_t simt_with_gemm_starts(maple_ctx* ctx, const DescentParams& p) {
+    cudaStream_t s = ctx->stream;
+    if (!ctx->cublas) {
+        if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    }
+    if (cublasSetStream(ctx->cublas, s) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    const int n = ctx->n, d = ctx->d;
+    const int64_t ch = std::min<int64_t>(p.count, kGemmStartsChunk);
+    cudaError_t e;
+    if ((e = ctx->g0buf.ensure((size_t)ch * n * 8)) != cudaSuccess) return e;
+    if (!p.Z0_out && (e = ctx->z0buf.ensure((size_t)ch * d * 8)) != cudaSuccess) return e;
+    const double one = 1.0, zero = 0.0;
+    for (int64_t off = 0; off < p.count; off += ch) {
+        DescentParams q = p;
+        q.begin = p.begin + off;
+        q.count = std::min(ch, p.count - off);
+        if (p.Z_out) q.Z_out = p.Z_out + off * d;
+        double* z0 = p.Z0_out ? p.Z0_out + off * d : ctx->z0buf.as<double>();
+        if ((e = launch_start_g0(q, ctx->g0buf.as<double>(), s)) != cudaSuccess) return e;
+        // column-major: Z0^T (d x cnt) = (B+ as n x d col-major)^T (G0^T: n x cnt col-major)
+        if (cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, d, (int)q.count, n, &one, p.Bp, n,
+                        ctx->g0buf.as<double>(), n, &zero, z0, d) != CUBLAS_STATUS_SUCCESS)
+            return cudaErrorUnknown;
+        q.Z0_in = z0;
+        q.Z0_out = nullptr;
+        if ((e = launch_descent_simt(q, s)) != cudaSuccess) return e;
+        ctx->launches += 2;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t run_descent(maple_ctx* ctx, const DescentParams& p) {
     ctx->launches++;
     switch (which_descent(ctx)) {
         case 2: return launch_descent_tc(p, ctx->stream);
         case 4: return launch_descent_tcp(p, ctx->stream);
-        default: return launch_descent_simt(p, ctx->stream);
+        default:
+            if ((int64_t)ctx->n * ctx->d >= kGemmStartsMinND) return simt_with_gemm_starts(ctx, p);
+            return launch_descent_simt(p, ctx->stream);
     }
 }
 
@@ -788,7 +830,7 @@ void maple_destroy(maple_ctx* ctx) {
                       &ctx->ell_f, &ctx->ell_own_f, &ctx->ell_fix, &ctx->ell_fixpos, &ctx->ell_b, &ctx->ell_owned, &ctx->ell_pos_s, &ctx->ell_pos_z, &ctx->AT_ptr, &ctx->AT_row,
                       &ctx->AT_val, &ctx->fb, &ctx->frows, &ctx->fX, &ctx->step_tab, &ctx->cand,
                       &ctx->keys, &ctx->idx, &ctx->pool, &ctx->counters, &ctx->flags, &ctx->codes, &ctx->sig, &ctx->ffreq, &ctx->fkey, &ctx->fbh, &ctx->fbs, &ctx->fbc, &ctx->flrow, &ctx->flsig, &ctx->l1,
-                      &ctx->fgc, &ctx->fgs, &ctx->fgr, &ctx->fhf,
+                      &ctx->fgc, &ctx->fgs, &ctx->fgr, &ctx->fhf, &ctx->g0buf, &ctx->z0buf,
                       &ctx->hist, &ctx->level_start, &ctx->cursor, &ctx->order, &ctx->keep, &ctx->witness,
                       &ctx->tmp_rows, &ctx->sortkeys, &ctx->sidx0, &ctx->sidx1, &ctx->zout, &ctx->z0out,
                       &ctx->aQ, &ctx->ac, &ctx->ac0, &ctx->aqg, &ctx->aX, &ctx->aF2, &ctx->aIt, &ctx->axb,
@@ -797,6 +839,7 @@ void maple_destroy(maple_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->stage_aug.release();
     ctx->stage_tab.release();
+    if (ctx->cublas) cublasDestroy(ctx->cublas);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;

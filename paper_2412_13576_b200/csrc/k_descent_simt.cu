@@ -139,6 +139,11 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
     // warp takes the dot products of its own start with them: B+ is read from L2 once per block instead of
     // once per start (C3: 672 KB per start before). Each dot product: lanes stride k, fixed-order reduction.
     for (int k = lane; k < QD * 32; k += 32) zsh[k] = 0.f;   // unused places hold z = 0 forever
+    __syncwarp();
+    if (p.Z0_in) {   // starts precomputed by a DGEMM on the host side of the launch (large n d)
+        if (active)
+            for (int j = lane; j < d; j += 32) zsh[sb.pos_z[j]] = (float)p.Z0_in[local * d + j];
+    } else {
     if (active)
         for (int k = lane; k < n; k += 32) g0sh[k] = start_coord(counter_uniform(p.seed, gi, k, n), p.lo[k], p.hi[k]);
     __syncwarp();
@@ -165,6 +170,7 @@ __global__ void __launch_bounds__(QD > 16 ? 512 : 1024, 1) descent_simt_kernel(c
             }
         }
         __syncthreads();
+    }
     }
     for (int k = threadIdx.x; k < Lf * 32; k += blockDim.x) ellf[k] = sb.ell_f[k];
     for (int k = threadIdx.x; k < Lb * 32; k += blockDim.x) ellb[k] = sb.ell_b[k];
@@ -346,7 +352,24 @@ cudaError_t launch_qd(const DescentParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+__global__ void start_g0_kernel(const DescentParams p, double* __restrict__ g0) {
+    const int n = p.n;
+    const int64_t total = p.count * n;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e / n;
+        const int k = (int)(e - s * n);
+        g0[e] = start_coord(counter_uniform(p.seed, p.begin + s, k, n), p.lo[k], p.hi[k]);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_start_g0(const DescentParams& p, double* g0, cudaStream_t s) {
+    if (p.count <= 0) return cudaSuccess;
+    const int64_t total = p.count * p.n;
+    start_g0_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 32), 256, 0, s>>>(p, g0);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s) {
     if (p.count <= 0) return cudaSuccess;

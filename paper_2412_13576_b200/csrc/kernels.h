@@ -48,6 +48,7 @@ struct DescentParams {
     unsigned long long* cand_count;
     float* Z_out;                 // optional: final iterates (count x d)
     double* Z0_out;               // optional: starts (count x d)
+    const double* Z0_in;          // optional (SIMT): the starts z0 = B+ g0 precomputed by a DGEMM (count x d, fp64)
     // CTA-pair tcgen05 kernel (k_descent_tcp.cu): padded operand copies of B and the range flag
     int tcp_np, tcp_dp;           // padded n (multiple of 64) and d (multiple of 96 / 32, see tcp_shape)
     const uint16_t* B16p;         // B as IEEE half, tcp_np x tcp_dp row-major (zero padded)
@@ -59,6 +60,8 @@ struct DescentParams {
 
 // SIMT descent + harvest (one warp per start). Returns a cudaError_t.
 cudaError_t launch_descent_simt(const DescentParams& p, cudaStream_t s);
+// g0 (count x n, fp64) of global starts [begin, begin + count): the same counter RNG and box map as the kernels
+cudaError_t launch_start_g0(const DescentParams& p, double* g0, cudaStream_t s);
 // tcgen05 descent + harvest (128 starts per CTA, state resident on chip). Returns cudaErrorNotSupported
 // when the shape does not fit the kernel's tile limits.
 cudaError_t launch_descent_tc(const DescentParams& p, cudaStream_t s);
