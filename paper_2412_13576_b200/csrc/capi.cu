@@ -292,6 +292,8 @@ FilterWork make_filter_work(maple_ctx* ctx, int algo) {
                   ctx->fbc.as<int32_t>() + (size_t)ctx->n * (ctx->Lh + 1), ctx->fgc.as<int32_t>(),
                   ctx->fgs.as<int32_t>(), ctx->fgr.as<int32_t>(), ctx->fhf.as<int32_t>(),
                   (int64_t)(ctx->fgr.bytes / 4), 0, 0, 0};
+    // test hook: MAPLE_GL_CAP caps the G-list capacity so the level pass's fallback (the indexed pass) is exercised
+    if (const char* cap = getenv("MAPLE_GL_CAP")) fw.gl_cap = std::min<int64_t>(fw.gl_cap, atoll(cap));
     return fw;
 }
 

@@ -313,3 +313,21 @@ def test_variant_c1_sets_within_closed_form(gpu_lib):
             rows = ctx.extract(1024, inst.steps, inst.lr, inst.seed).rows()
             assert np.all(OP.check_rows(inst.A, inst.l, inst.u, rows))
             assert _set(rows) <= expected
+
+
+@pytest.mark.parametrize("name,N", [("C2b", 8192), ("C3", 4096)])
+def test_level_filter_fallback_identical(gpu_lib, name, N, monkeypatch):
+    """The level-synchronous filter falls back to the indexed pass when its G lists exceed their capacity
+    (MAPLE_GL_CAP, a test hook, forces it): the kept set stays bit-identical to the indexed algorithm."""
+    from synth import config
+    inst = config(name)
+    ctx = _ctx(gpu_lib, inst)
+    ctx.set_filter_algorithm(2)
+    ref = ctx.extract(N, inst.steps, inst.lr, inst.seed).rows()
+    ctx.set_filter_algorithm(3)
+    monkeypatch.setenv("MAPLE_GL_CAP", "1")
+    forced = ctx.extract(N, inst.steps, inst.lr, inst.seed).rows()
+    monkeypatch.delenv("MAPLE_GL_CAP")
+    normal = ctx.extract(N, inst.steps, inst.lr, inst.seed).rows()
+    np.testing.assert_array_equal(forced, ref)
+    np.testing.assert_array_equal(normal, ref)
