@@ -265,7 +265,7 @@ int prepare_set(maple_ctx* ctx, int64_t cand_cap, int64_t pool_cap, int filter_m
             CU(ctx->fgc.ensure(nbins * 4));
             CU(ctx->fgs.ensure((nbins + 1) * 4));
             CU(ctx->fgr.ensure(std::min<size_t>((size_t)ctx->pool_cap * std::min(ctx->n, kGlEntriesPerRow), kGlMaxEntries) * 4));
-            CU(ctx->fhf.ensure((size_t)ctx->n * 4 + 8));   // + the level kernel's grid barrier words
+            CU(ctx->fhf.ensure((size_t)ctx->n * 4 + 8 + (size_t)(ctx->Lh + 2) * 4));   // + barrier words, work counters
         }
     }
     CU(cudaMemsetAsync(ctx->keys.p, 0, ctx->table_slots * 8, ctx->stream));

@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kIdxThreads) dominance_idx_kernel(FilterWork f
 // coordinate's list. The pairs are blocked coordinate-major: a work item is (c, 256 rows g of level L with
 // c ∈ supp(g), a segment of c's list), the list tiles staged in shared memory and shared by the 256 rows.
 // The keep bit is defined pairwise, so it equals the other algorithms' (only the witness may differ).
-constexpr int kLvThreads = 256, kLvTile = 512, kLvSeg = 4096;
+constexpr int kLvThreads = 256, kLvTile = 512, kLvSeg = 512;
 
 // G lists: every undecided row g (keep == 2) is filed under bin L1(g) n + c for each c ∈ supp(g);
 // pass 0 counts (gl_cursor as histogram), pass 1 scatters (gl_cursor as cursor)
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(1024) scan_bins_kernel(const int32_t* n_undec,
 // over P_h's bits of the P masks and over N_h's bits of the N masks), h ⊑ -g_j the same with P and N of g exchanged.
 // So one lane tests h against 32 rows at once and stops as soon as no row survives (usually after a few bits); the
 // surviving (h, g_j) pairs get the exact test on the full codes.
-__device__ void level_tile(const FilterWork& fw, int L) {
+__device__ void level_tile(const FilterWork& fw, int L, int32_t* work) {
     constexpr int NWARP = kLvThreads / 32;
     __shared__ int32_t pre[kIdxMaxN + 1];
     __shared__ uint4 tsig[kLvTile];
@@ -713,7 +713,11 @@ __device__ void level_tile(const FilterWork& fw, int L) {
     }
     const int32_t total = pre[n];
     volatile uint8_t* vkeep = fw.keep;
-    for (int32_t item = blockIdx.x; item < total; item += gridDim.x) {
+    // items are taken dynamically (one atomic per item per block): their cost varies with how soon rows die
+    __shared__ int32_t s_item;
+    if (tid == 0) s_item = atomicAdd(work, 1);
+    __syncthreads();
+    for (int32_t item = s_item; item < total;) {
         int lo = 0, hi = n;   // the coordinate c with pre[c] <= item < pre[c + 1]
         while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -805,6 +809,9 @@ __device__ void level_tile(const FilterWork& fw, int L) {
             }
         }
         __syncthreads();   // the tile buffers and masks are reused by the next item
+        if (tid == 0) s_item = atomicAdd(work, 1);
+        __syncthreads();
+        item = s_item;
     }
 }
 
@@ -858,7 +865,7 @@ __global__ void __launch_bounds__(kLvThreads) level_filter_kernel(FilterWork fw,
         if (fw.level_start[L] == fw.level_start[L + 1]) continue;   // no row has L1 = L
         if (fw.gl_start[(size_t)(L + 1) * n] > fw.gl_start[(size_t)L * n]) {
             grid_barrier(bar, bar + 1);
-            level_tile(fw, L);
+            level_tile(fw, L, reinterpret_cast<int32_t*>(bar + 2) + L);
             grid_barrier(bar, bar + 1);
         }
         level_append(fw, L);
@@ -1140,8 +1147,9 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         const int grid = std::max(1, per_sm) * nsm;
-        unsigned* bar = reinterpret_cast<unsigned*>(fw.h_fill + fw.n);   // 2 words after the fill counters
-        if ((e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s)) != cudaSuccess) return e;
+        // after the fill counters: 2 grid-barrier words, then one work counter per level
+        unsigned* bar = reinterpret_cast<unsigned*>(fw.h_fill + fw.n);
+        if ((e = cudaMemsetAsync(bar, 0, (2 + fw.Lmax + 2) * sizeof(unsigned), s)) != cudaSuccess) return e;
         void* args[] = {&fw, &bar};
         if ((e = cudaLaunchCooperativeKernel((void*)level_filter_kernel, grid, kLvThreads, args, 0, s)) != cudaSuccess)
             return e;
