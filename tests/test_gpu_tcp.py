@@ -115,3 +115,15 @@ def test_tcp_sets_gate_g3(gpu_lib, c3):
     diff = np.array(sorted(g ^ m64), dtype=np.int64).reshape(-1, c3.n)
     if diff.size:
         assert np.all(OP.check_rows(c3.A, c3.l, c3.u, diff))
+
+
+def test_tcp_range_overflow_falls_back_to_simt(gpu_lib, c3):
+    """An iterate beyond the f16 operand range of the CTA-pair kernel (|z| > 1023, here from a huge step size) sets
+    its device flag; the extraction is redone on the SIMT kernel, so the result equals a SIMT-only context's."""
+    lr = 500.0
+    a = _ctx(gpu_lib, c3, TCP)
+    b = _ctx(gpu_lib, c3, SIMT)
+    ra = a.extract(512, 20, lr, c3.seed).rows()
+    rb = b.extract(512, 20, lr, c3.seed).rows()
+    assert a.descent_kernel == "simt"        # the context remembers the overflow
+    np.testing.assert_array_equal(ra, rb)
