@@ -53,9 +53,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=max(1, min(8, len(jobs)))) as ex:
         logs = list(ex.map(_run, jobs))
     if jobs or force or _stale(OUT, objs):
-        _run([NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lcudart_static", "-lcublas", "-Xlinker",
-                                                              "-rpath,/usr/local/cuda/lib64", "-lrt", "-ldl",
-                                                              "-lpthread"])
+        _run([NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     if verbose:
         for lg in logs:
             sys.stdout.write(lg)

@@ -4,6 +4,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cublas_v2.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cmath>
@@ -602,12 +603,41 @@ int ensure_descent_operands(maple_ctx* ctx) {
 constexpr int64_t kGemmStartsMinND = 200000;
 constexpr int64_t kGemmStartsChunk = 65536;
 
+// cuBLAS is opened on first use (dlopen), so processes that never take this path (every shape but C5's) do not
+// pay its module registration when they create their first context
+struct CublasApi {
+    bool tried = false, ok = false;
+    cublasStatus_t (*create)(cublasHandle_t*) = nullptr;
+    cublasStatus_t (*destroy)(cublasHandle_t) = nullptr;
+    cublasStatus_t (*set_stream)(cublasHandle_t, cudaStream_t) = nullptr;
+    cublasStatus_t (*dgemm)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int, const double*,
+                            const double*, int, const double*, int, const double*, double*, int) = nullptr;
+};
+CublasApi& cublas_api() {
+    static CublasApi api;
+    if (!api.tried) {
+        api.tried = true;
+        void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("/usr/local/cuda/lib64/libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.create = reinterpret_cast<decltype(api.create)>(dlsym(h, "cublasCreate_v2"));
+            api.destroy = reinterpret_cast<decltype(api.destroy)>(dlsym(h, "cublasDestroy_v2"));
+            api.set_stream = reinterpret_cast<decltype(api.set_stream)>(dlsym(h, "cublasSetStream_v2"));
+            api.dgemm = reinterpret_cast<decltype(api.dgemm)>(dlsym(h, "cublasDgemm_v2"));
+            api.ok = api.create && api.destroy && api.set_stream && api.dgemm;
+        }
+    }
+    return api;
+}
+
 cudaError_t simt_with_gemm_starts(maple_ctx* ctx, const DescentParams& p) {
     cudaStream_t s = ctx->stream;
+    CublasApi& cb = cublas_api();
+    if (!cb.ok) return launch_descent_simt(p, s);   // no cuBLAS: the kernel computes its starts itself
     if (!ctx->cublas) {
-        if (cublasCreate(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+        if (cb.create(&ctx->cublas) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
     }
-    if (cublasSetStream(ctx->cublas, s) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
+    if (cb.set_stream(ctx->cublas, s) != CUBLAS_STATUS_SUCCESS) return cudaErrorUnknown;
     const int n = ctx->n, d = ctx->d;
     const int64_t ch = std::min<int64_t>(p.count, kGemmStartsChunk);
     cudaError_t e;
@@ -622,8 +652,8 @@ cudaError_t simt_with_gemm_starts(maple_ctx* ctx, const DescentParams& p) {
         double* z0 = p.Z0_out ? p.Z0_out + off * d : ctx->z0buf.as<double>();
         if ((e = launch_start_g0(q, ctx->g0buf.as<double>(), s)) != cudaSuccess) return e;
         // column-major: Z0^T (d x cnt) = (B+ as n x d col-major)^T (G0^T: n x cnt col-major)
-        if (cublasDgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, d, (int)q.count, n, &one, p.Bp, n,
-                        ctx->g0buf.as<double>(), n, &zero, z0, d) != CUBLAS_STATUS_SUCCESS)
+        if (cb.dgemm(ctx->cublas, CUBLAS_OP_T, CUBLAS_OP_N, d, (int)q.count, n, &one, p.Bp, n,
+                     ctx->g0buf.as<double>(), n, &zero, z0, d) != CUBLAS_STATUS_SUCCESS)
             return cudaErrorUnknown;
         q.Z0_in = z0;
         q.Z0_out = nullptr;
@@ -841,7 +871,7 @@ void maple_destroy(maple_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->stage_aug.release();
     ctx->stage_tab.release();
-    if (ctx->cublas) cublasDestroy(ctx->cublas);
+    if (ctx->cublas) cublas_api().destroy(ctx->cublas);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     delete ctx;

@@ -50,6 +50,7 @@ __global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, 
 }
 
 // q_e = g_e^T Q g_e for every direction of D (per instance), over the nonzeros of g_e
+constexpr int kQgRegs = 24;   // directions with at most this many nonzeros keep their words in registers
 __global__ void qg_kernel(AugmentParams p) {
     const int nD = 2 * p.n_dir;
     const int64_t total = (int64_t)nD * p.n_inst;
@@ -59,14 +60,32 @@ __global__ void qg_kernel(AugmentParams p) {
         const double* Q = p.Q + (size_t)inst * p.n * p.n;
         const int k = p.nnz[e];
         double acc = 0.0;
-        for (int a = 0; a < k; ++a) {
-            const uint32_t wa = p.words[(size_t)a * nD + e];
-            double row = 0.0;
-            for (int b = 0; b < k; ++b) {
-                const uint32_t wb = p.words[(size_t)b * nD + e];
-                row += Q[(size_t)wcol(wa) * p.n + wcol(wb)] * (double)wval(wb);
+        if (k <= kQgRegs) {   // the direction's words read once (slot-major, coalesced over e), then k^2 Q reads
+            uint32_t w[kQgRegs];
+#pragma unroll
+            for (int a = 0; a < kQgRegs; ++a) w[a] = a < k ? p.words[(size_t)a * nD + e] : 0u;
+#pragma unroll
+            for (int a = 0; a < kQgRegs; ++a) {
+                if (a >= k) break;
+                const double* qa = Q + (size_t)wcol(w[a]) * p.n;
+                double row = 0.0;
+#pragma unroll
+                for (int b = 0; b < kQgRegs; ++b) {
+                    if (b >= k) break;
+                    row += qa[wcol(w[b])] * (double)wval(w[b]);   // the same order as below: bit-identical
+                }
+                acc += (double)wval(w[a]) * row;
             }
-            acc += (double)wval(wa) * row;
+        } else {
+            for (int a = 0; a < k; ++a) {
+                const uint32_t wa = p.words[(size_t)a * nD + e];
+                double row = 0.0;
+                for (int b = 0; b < k; ++b) {
+                    const uint32_t wb = p.words[(size_t)b * nD + e];
+                    row += Q[(size_t)wcol(wa) * p.n + wcol(wb)] * (double)wval(wb);
+                }
+                acc += (double)wval(wa) * row;
+            }
         }
         const_cast<double*>(p.qg)[(size_t)inst * nD + e] = acc;
     }
