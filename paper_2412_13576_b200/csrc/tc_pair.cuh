@@ -35,9 +35,15 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// arrive (release, cluster scope) on an mbarrier given by its shared::cluster address (possibly the peer's)
+// arrive on an mbarrier given by its shared::cluster address (possibly the peer's). Default semantics (release at
+// CTA scope: MEMBAR.ALL.CTA + the arrive). Every consumer of these barriers is an async-proxy operation (an MMA
+// reading this CTA's shared-memory operands or TMEM) issued after the wait, and every producer makes its data
+// visible to that proxy before arriving (fence.proxy.async for shared-memory operands, tcgen05.wait::ld +
+// tcgen05.fence::before_thread_sync for TMEM reads), so cluster-scope release adds nothing but its cost: it
+// compiles to MEMBAR.ALL.GPU + ERRBAR + CGAERRBAR, which waits for this warp's outstanding global stores (the
+// harvested rows) — 17 % of the CTA-pair kernel's stall samples in profiles/r2_ncu_descent_tcp_v7.md.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
 }
 
 // arrive on a local mbarrier and add `bytes` to its expected transaction count
