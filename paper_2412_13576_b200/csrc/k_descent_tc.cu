@@ -205,26 +205,31 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
         fence_proxy_async();
         fence_before();
         __syncthreads();  // B1: operands written, pair info visible
-        if (tid == 0) {
+        if (warp == 0) {   // warp 0 converged: descriptors in uniform registers, one elected lane issues + commits
             fence_after();
+            const bool leader = elect_one();
             if (do_fwd) {
 #pragma unroll
                 for (int kk = 0; kk < DP / 8; ++kk)
-                    mma_tf32(tbase + L::CG, desc(sZHI + kk * 2 * LBO_A, LBO_A, SBO),
-                             desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, kk > 0);
+                    if (leader)
+                        mma_tf32(tbase + L::CG, desc(sZHI + kk * 2 * LBO_A, LBO_A, SBO),
+                                 desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, kk > 0);
 #pragma unroll
                 for (int kk = 0; kk < DP / 8; ++kk)
-                    mma_tf32(tbase + L::CG, desc(sZLO + kk * 2 * LBO_A, LBO_A, SBO),
-                             desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, 1);
-                commit(&mbar[0]);
+                    if (leader)
+                        mma_tf32(tbase + L::CG, desc(sZLO + kk * 2 * LBO_A, LBO_A, SBO),
+                                 desc(sB32 + kk * 2 * LBO_N, LBO_N, SBO), ID_FWD, 1);
+                if (leader) commit(&mbar[0]);
             }
             if (do_harv) {   // committed separately: it runs while the sign epilogue reads G
 #pragma unroll
                 for (int kk = 0; kk < DP / 16; ++kk)
-                    mma_f16(tbase + L::CX, desc(sR + kk * 2 * LBO_A, LBO_A, SBO),
-                            desc(sB16 + kk * 2 * LBO_N, LBO_N, SBO), ID_HARV, kk > 0);
-                commit(&mbar[2]);
+                    if (leader)
+                        mma_f16(tbase + L::CX, desc(sR + kk * 2 * LBO_A, LBO_A, SBO),
+                                desc(sB16 + kk * 2 * LBO_N, LBO_N, SBO), ID_HARV, kk > 0);
+                if (leader) commit(&mbar[2]);
             }
+            __syncwarp();
         }
         if (do_fwd) {
 #ifndef MAPLE_TC_CTA_WAIT
@@ -317,13 +322,16 @@ __global__ void __launch_bounds__(kThreads, 2) descent_tc_kernel(const DescentPa
         fence_proxy_async();
         fence_before();
         __syncthreads();  // B2: S and both halves' harvest tests written; G consumed (Γ reuses its columns)
-        if (do_fwd && tid == 0) {
+        if (do_fwd && warp == 0) {
             fence_after();
+            const bool leader = elect_one();
 #pragma unroll
             for (int kk = 0; kk < NP / 16; ++kk)
-                mma_f16(tbase + L::CG, desc(sS + kk * 2 * LBO_A, LBO_A, SBO), desc(sBT + kk * 2 * LBO_D, LBO_D, SBO),
-                        ID_BWD, kk > 0);
-            commit(&mbar[1]);
+                if (leader)
+                    mma_f16(tbase + L::CG, desc(sS + kk * 2 * LBO_A, LBO_A, SBO),
+                            desc(sBT + kk * 2 * LBO_D, LBO_D, SBO), ID_BWD, kk > 0);
+            if (leader) commit(&mbar[1]);
+            __syncwarp();
         }
         if (do_harv && warp_harv) {
             // ---- candidate rows (overlaps the backward MMA): both halves passed the box test, g != 0 ----
