@@ -1466,6 +1466,7 @@ int maple_feasible_starts(maple_ctx* ctx, const int32_t* b, int32_t k, int32_t s
     p.omb2 = (float)(1.0 - ctx->beta2);
     p.step_tab = ctx->step_tab.as<float4>();
     p.seed = seed;
+    p.nnz = ctx->nnz;
     p.A_rowptr = ctx->A_rowptr.as<int32_t>();
     p.A_col = ctx->A_col.as<int32_t>();
     p.A_val = ctx->A_val.as<int32_t>();

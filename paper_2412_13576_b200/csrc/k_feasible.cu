@@ -21,9 +21,26 @@ template <int QN>
 __global__ void __launch_bounds__(kWarps * 32, 1) feasible_kernel(const FeasibleParams p) {
     extern __shared__ __align__(16) unsigned char fsm[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int n = p.n, m = p.m;
+    const int n = p.n, m = p.m, nnz = p.nnz;
     float* xsh = reinterpret_cast<float*>(fsm) + (size_t)wid * (n + m);
     float* rsh = xsh + n;
+    // A's CSR and CSC staged once per block (every step of every warp walks them: from global memory each
+    // dependent index load was an L1/L2 round trip on the step's critical path)
+    int32_t* a_rp = reinterpret_cast<int32_t*>(fsm + (size_t)kWarps * (n + m) * 4);
+    int32_t* a_col = a_rp + (m + 1);
+    int32_t* a_val = a_col + nnz;
+    int32_t* t_cp = a_val + nnz;
+    int32_t* t_row = t_cp + (n + 1);
+    int32_t* t_val = t_row + nnz;
+    for (int i = threadIdx.x; i <= m; i += blockDim.x) a_rp[i] = p.A_rowptr[i];
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) t_cp[i] = p.AT_colptr[i];
+    for (int i = threadIdx.x; i < nnz; i += blockDim.x) {
+        a_col[i] = p.A_col[i];
+        a_val[i] = p.A_val[i];
+        t_row[i] = p.AT_row[i];
+        t_val[i] = p.AT_val[i];
+    }
+    __syncthreads();
     const int64_t s = (int64_t)blockIdx.x * kWarps + wid;
     if (s >= p.k) return;
     const uint64_t seed = p.seed ^ kFeasSalt;
@@ -46,7 +63,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) feasible_kernel(const Feasible
         // residual r = A x - b (lanes over rows of A)
         for (int a = lane; a < m; a += 32) {
             float acc = -(float)p.b[a];
-            for (int e = p.A_rowptr[a]; e < p.A_rowptr[a + 1]; ++e) acc = fmaf((float)p.A_val[e], xsh[p.A_col[e]], acc);
+            for (int e = a_rp[a]; e < a_rp[a + 1]; ++e) acc = fmaf((float)a_val[e], xsh[a_col[e]], acc);
             rsh[a] = acc;
         }
         __syncwarp();
@@ -56,7 +73,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) feasible_kernel(const Feasible
             const int j = lane + 32 * q;
             if (j < n) {
                 float acc = 0.f;  // (A^T r)_j over the nonzeros of column j
-                for (int e = p.AT_colptr[j]; e < p.AT_colptr[j + 1]; ++e) acc = fmaf((float)p.AT_val[e], rsh[p.AT_row[e]], acc);
+                for (int e = t_cp[j]; e < t_cp[j + 1]; ++e) acc = fmaf((float)t_val[e], rsh[t_row[e]], acc);
                 const float xx = x[q];
                 const float g = 2.f * acc + p.lam3 * (ceilf(xx) + floorf(xx) - 2.f * xx);
                 mm[q] = p.beta1 * mm[q] + p.omb1 * g;
@@ -79,8 +96,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) feasible_kernel(const Feasible
     bool ok = true;
     for (int a = lane; a < m; a += 32) {
         long long acc = -(long long)p.b[a];
-        for (int e = p.A_rowptr[a]; e < p.A_rowptr[a + 1]; ++e)
-            acc += (long long)p.A_val[e] * (long long)xsh[p.A_col[e]];
+        for (int e = a_rp[a]; e < a_rp[a + 1]; ++e)
+            acc += (long long)a_val[e] * (long long)xsh[a_col[e]];
         ok &= acc == 0;
     }
     ok = __all_sync(0xffffffffu, ok);
@@ -100,7 +117,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) feasible_kernel(const Feasible
 
 template <int QN>
 cudaError_t launch_qn(const FeasibleParams& p, cudaStream_t s) {
-    const size_t smem = (size_t)kWarps * (p.n + p.m) * 4;
+    const size_t smem = (size_t)kWarps * (p.n + p.m) * 4 + (size_t)(p.m + 1 + p.n + 1 + 4 * (size_t)p.nnz) * 4;
     cudaError_t e = cudaFuncSetAttribute(feasible_kernel<QN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t blocks = (p.k + kWarps - 1) / kWarps;

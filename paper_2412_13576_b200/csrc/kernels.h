@@ -163,6 +163,7 @@ struct FeasibleParams {
     float lam3, beta1, beta2, eps, omb1, omb2;
     const float4* step_tab;
     uint64_t seed;
+    int nnz;                      // nonzeros of A (the CSR / CSC arrays below are staged in shared memory)
     const int32_t* A_rowptr;      // CSR of A
     const int32_t* A_col;
     const int32_t* A_val;
