@@ -51,12 +51,15 @@ __global__ void ell_fill_kernel(const int8_t* __restrict__ dirs, int nD, int n, 
 
 // q_e = g_e^T Q g_e for every direction of D (per instance), over the nonzeros of g_e
 constexpr int kQgRegs = 24;   // directions with at most this many nonzeros keep their words in registers
+// D is sorted and closed under negation with D[nD-1-e] = -D[e] (signed_merge_kernel), and q(-g) = q(g) bit for bit
+// (negation is exact and commutes with every product and sum below), so each thread computes e < nD/2 and writes
+// both entries
 __global__ void qg_kernel(AugmentParams p) {
-    const int nD = 2 * p.n_dir;
-    const int64_t total = (int64_t)nD * p.n_inst;
+    const int nD = 2 * p.n_dir, half = p.n_dir;
+    const int64_t total = (int64_t)half * p.n_inst;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int inst = (int)(t / nD);
-        const int e = (int)(t % nD);
+        const int inst = (int)(t / half);
+        const int e = (int)(t % half);
         const double* Q = p.Q + (size_t)inst * p.n * p.n;
         const int k = p.nnz[e];
         double acc = 0.0;
@@ -88,6 +91,7 @@ __global__ void qg_kernel(AugmentParams p) {
             }
         }
         const_cast<double*>(p.qg)[(size_t)inst * nD + e] = acc;
+        const_cast<double*>(p.qg)[(size_t)inst * nD + (nD - 1 - e)] = acc;
     }
 }
 
@@ -326,7 +330,7 @@ cudaError_t launch_augment_best(const AugmentParams& p, int32_t* xbest, double* 
 
 cudaError_t launch_augment_qg(const AugmentParams& p, cudaStream_t s) {
     if (p.table) return cudaSuccess;   // tables: no quadratic form
-    const int64_t total = (int64_t)2 * p.n_dir * p.n_inst;
+    const int64_t total = (int64_t)p.n_dir * p.n_inst;   // one thread per (instance, direction pair g, -g)
     if (total <= 0) return cudaSuccess;
     int64_t blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

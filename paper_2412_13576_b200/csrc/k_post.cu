@@ -1038,25 +1038,27 @@ __device__ __forceinline__ int lex_cmp_signed(const int8_t* a, const int8_t* b, 
 }
 
 // D = S ∪ -S in lexicographic order, from S sorted ascending: negation reverses the order, so -S ascending is
-// N[j] = -S[k-1-j], and no row of S equals a row of -S (canonical rows have a positive first nonzero). Each row
-// goes to its own index plus its rank in the other sequence (binary search): a merge, no sort.
+// N[j] = -S[k-1-j], and no row of S equals a row of -S (canonical rows have a positive first nonzero). Row i of S
+// goes to i plus its rank in N (binary search): a merge, no sort. D is closed under negation and negation reverses
+// the order, so D[2k-1-e] = -D[e]: the same thread writes -S[i] at 2k-1-(i + rank) (half the searches).
 __global__ void signed_merge_kernel(const int8_t* __restrict__ S, int64_t k, int n, int n_pad, int8_t* out) {
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * k; t += (int64_t)gridDim.x * blockDim.x) {
-        const bool from_neg = t >= k;
-        const int64_t i = from_neg ? t - k : t;                 // index within its own ascending sequence
-        const int8_t* self = from_neg ? S + (size_t)(k - 1 - i) * n_pad : S + (size_t)i * n_pad;
-        // rank: number of rows of the other sequence that are smaller than this row (as signed rows)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x) {
+        const int8_t* self = S + (size_t)i * n_pad;
+        // rank: number of rows of N smaller than S[i]
         int64_t lo = 0, hi = k;
         while (lo < hi) {
             const int64_t mid = (lo + hi) >> 1;
-            // c = cmp(other[mid], this row)
-            const int c = from_neg ? lex_cmp_signed(S + (size_t)mid * n_pad, self, true, n)          // S[mid] vs -self
-                                   : -lex_cmp_signed(self, S + (size_t)(k - 1 - mid) * n_pad, true, n);  // N[mid] vs self
+            const int c = -lex_cmp_signed(self, S + (size_t)(k - 1 - mid) * n_pad, true, n);   // N[mid] vs self
             if (c < 0) lo = mid + 1;
             else hi = mid;
         }
-        int8_t* dst = out + (size_t)(i + lo) * n_pad;
-        for (int q = 0; q < n_pad; ++q) dst[q] = from_neg ? (int8_t)(-self[q]) : self[q];
+        const int64_t pos = i + lo;
+        int8_t* dp = out + (size_t)pos * n_pad;
+        int8_t* dn = out + (size_t)(2 * k - 1 - pos) * n_pad;
+        for (int q = 0; q < n_pad; ++q) {
+            dp[q] = self[q];
+            dn[q] = (int8_t)(-self[q]);
+        }
     }
 }
 
@@ -1192,7 +1194,7 @@ cudaError_t launch_filter(const unsigned long long* dcount, int64_t cap, const u
 
 cudaError_t launch_signed_merge(const int8_t* S, int64_t k, int n, int n_pad, int8_t* out, cudaStream_t s) {
     if (k <= 0) return cudaSuccess;
-    signed_merge_kernel<<<grid_for(2 * k), 256, 0, s>>>(S, k, n, n_pad, out);
+    signed_merge_kernel<<<grid_for(k), 256, 0, s>>>(S, k, n, n_pad, out);
     return cudaGetLastError();
 }
 
