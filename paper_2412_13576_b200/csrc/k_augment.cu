@@ -18,6 +18,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_pair.cuh"   // cluster rank / barrier / mapa (the split augmentation)
 
 namespace maple {
 
@@ -107,16 +108,31 @@ __device__ __forceinline__ bool better(const Cand& a, const Cand& b) {
     return a.lam < b.lam;
 }
 
+// a cluster peer's Cand (shared::cluster load of the same variable in CTA `rank`)
+__device__ __forceinline__ Cand ld_peer_cand(const Cand* local, uint32_t rank) {
+    const uint32_t ra = pair::mapa((uint32_t)__cvta_generic_to_shared(local), rank);
+    unsigned long long k;
+    int e, l;
+    asm volatile("ld.shared::cluster.b64 %0, [%1];" : "=l"(k) : "r"(ra) : "memory");
+    asm volatile("ld.shared::cluster.b32 %0, [%1+8];" : "=r"(e) : "r"(ra) : "memory");
+    asm volatile("ld.shared::cluster.b32 %0, [%1+12];" : "=r"(l) : "r"(ra) : "memory");
+    return Cand{__longlong_as_double((long long)k), e, l};
+}
+
 __global__ void __launch_bounds__(kAugThreads, 1)
-augment_kernel(AugmentParams p, int staged) {
+augment_kernel(AugmentParams p, int staged, int split) {
     __shared__ int32_t x[kMaxN];
     __shared__ int32_t up[kMaxN], dn[kMaxN];   // room to the bounds: u - x, x - l
     __shared__ double grad[kMaxN];
     __shared__ Cand wbest[kAugThreads / 32];
     __shared__ Cand best_sh;
     __shared__ double f2_sh;
+    __shared__ Cand split_best[2];   // this CTA's best of iteration it, in slot it & 1 (read by the cluster peers)
     extern __shared__ __align__(16) unsigned char dsm[];   // staged D (ELL) + q_g when it fits
-    const int inc = blockIdx.x;  // incumbent index over all instances
+    // split > 1: the incumbent's directions are scanned by a cluster of `split` CTAs (few incumbents would leave
+    // SMs idle); each CTA keeps the full state and applies the same best step, combined through DSMEM
+    const int inc = blockIdx.x / split;  // incumbent index over all instances
+    const int crank = split > 1 ? (int)pair::cluster_rank() : 0;
     const int inst = inc / p.k0;
     const int n = p.n;
     const double* Q = p.Q + (size_t)inst * n * n;
@@ -166,7 +182,7 @@ augment_kernel(AugmentParams p, int staged) {
     int it = 0;
     for (; it < p.max_iter; ++it) {
         Cand mine{DBL_MAX, 0x7fffffff, 0x7fffffff};
-        for (int e = threadIdx.x; e < nD; e += blockDim.x) {
+        for (int e = threadIdx.x + crank * blockDim.x; e < nD; e += split * blockDim.x) {
             // step bound first, leaving at the first blocked coordinate (in a box most directions are blocked at
             // an incumbent: a binary box blocks every g with a coordinate pushing past 0 or 1), then the score
             const uint32_t* we = p.words + e;
@@ -228,6 +244,19 @@ augment_kernel(AugmentParams p, int staged) {
             for (int w = 1; w < (int)(blockDim.x / 32); ++w)
                 if (better(wbest[w], b)) b = wbest[w];
             best_sh = b;
+            if (split > 1) split_best[it & 1] = b;
+        }
+        if (split > 1) {   // combine the cluster's bests (better() is a strict total order: every CTA gets the same)
+            pair::cluster_sync();
+            if (threadIdx.x == 0) {
+                Cand b = best_sh;
+                for (int r = 0; r < split; ++r)
+                    if (r != crank) {
+                        const Cand o = ld_peer_cand(&split_best[it & 1], (uint32_t)r);
+                        if (better(o, b)) b = o;
+                    }
+                best_sh = b;
+            }
         }
         __syncthreads();
         const Cand b = best_sh;
@@ -254,6 +283,8 @@ augment_kernel(AugmentParams p, int staged) {
         if (threadIdx.x == 0) f2_sh += b.key;
         __syncthreads();
     }
+    if (split > 1) pair::cluster_sync();   // the peers' last reads of split_best are done before any CTA exits
+    if (crank != 0) return;
     for (int i = threadIdx.x; i < n; i += blockDim.x) xg[i] = x[i];
     if (threadIdx.x == 0) {
         p.F2[inc] = f2_sh;
@@ -350,8 +381,28 @@ cudaError_t launch_augment(const AugmentParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     const int threads = nD2 > 16384 ? kAugThreads : 256;
-    augment_kernel<<<(unsigned)blocks, threads, staged ? smem : 0, s>>>(p, staged);
-    return cudaGetLastError();
+    // few incumbents with a large D (C3: ~100 incumbents, |D| = 1.6 M): a cluster of `split` CTAs of 256 threads per
+    // incumbent (four fit an SM), as many as one wave holds, so that every SM scans and each thread scans fewer
+    // directions; otherwise one CTA per incumbent
+    int split = 1;
+    if (threads == kAugThreads && blocks < 148) split = (int)std::min<int64_t>(8, (4 * 148) / blocks);
+    if (split <= 1) {
+        augment_kernel<<<(unsigned)blocks, threads, staged ? smem : 0, s>>>(p, staged, 1);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(blocks * split));
+    cfg.blockDim = dim3(kAugThreads / 4);
+    cfg.dynamicSmemBytes = staged ? smem : 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)split;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, augment_kernel, p, staged, split);
 }
 
 }  // namespace maple
