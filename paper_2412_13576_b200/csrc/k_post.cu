@@ -1053,11 +1053,14 @@ __global__ void signed_merge_kernel(const int8_t* __restrict__ S, int64_t k, int
             else hi = mid;
         }
         const int64_t pos = i + lo;
-        int8_t* dp = out + (size_t)pos * n_pad;
-        int8_t* dn = out + (size_t)(2 * k - 1 - pos) * n_pad;
-        for (int q = 0; q < n_pad; ++q) {
-            dp[q] = self[q];
-            dn[q] = (int8_t)(-self[q]);
+        // rows are n_pad bytes, n_pad a multiple of 16: 16-byte copies, bytewise negation (mod 256, as int8_t(-v))
+        const uint4* src = reinterpret_cast<const uint4*>(self);
+        uint4* dp = reinterpret_cast<uint4*>(out + (size_t)pos * n_pad);
+        uint4* dn = reinterpret_cast<uint4*>(out + (size_t)(2 * k - 1 - pos) * n_pad);
+        for (int q = 0; q < n_pad / 16; ++q) {
+            const uint4 v = src[q];
+            dp[q] = v;
+            dn[q] = make_uint4(__vneg4(v.x), __vneg4(v.y), __vneg4(v.z), __vneg4(v.w));
         }
     }
 }
